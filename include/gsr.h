@@ -1,0 +1,198 @@
+/*
+ * gsr.h -- C-ABI of the B200-native 2DGS camera + LiDAR renderer
+ *          (hot path of arXiv 2503.11731, §III-A).
+ *
+ *   gs_project  ->  gs_bin_sort  ->  gs_render_camera | gs_render_lidar
+ *
+ * Conventions for every entry point
+ *   - Ownership: the caller owns every buffer.  The library never allocates,
+ *     keeps no global state and holds no pointer after a call returns.
+ *   - Memory: pointers named d_* and all array pointers inside gs_surfels and
+ *     the output/work buffers are DEVICE pointers (cudaMalloc / torch);
+ *     gs_sensor.beam_elevation is a HOST pointer (copied into kernel
+ *     parameters).  Structs themselves are host memory, read during the call.
+ *   - Asynchrony: all device work is enqueued on `stream` (a cudaStream_t; 0
+ *     = legacy default stream).  No call synchronises the device.
+ *   - Errors: arguments are validated synchronously on the host before any
+ *     launch: GS_ERR_CONFIG (null required pointer, wrong sensor kind for the
+ *     call, sh_degree outside 0..3, width/height < 1, buffer too small),
+ *     GS_ERR_RANGE (focal <= 0, non-monotone beam table, azimuth span outside
+ *     (0, 2pi], theta_max outside (0, pi), tile shape outside 1..1024
+ *     threads), GS_ERR_CUDA (launch failure, from cudaGetLastError).  On any
+ *     error nothing is enqueued after the failing launch; gs_last_error()
+ *     returns a thread-local message.  Non-finite surfel inputs are not an
+ *     error: such surfels are culled.
+ *   - Reentrancy: calls are pure functions of their inputs; concurrent calls
+ *     on different streams with distinct output buffers are safe.
+ *   - Determinism: no floating-point atomics; outputs are bitwise
+ *     reproducible for identical inputs, independent of tile shape.
+ *
+ * Sizing protocol (the pair count P is only known on the device):
+ *   simple mode: gs_project, synchronise, read *d_num_pairs, allocate P
+ *   pairs, gs_bin_sort.  Graph mode: pass a pair_capacity up front; if
+ *   P > pair_capacity gs_bin_sort sets *d_overflow = 1, leaves keys/values/
+ *   tile_ranges undefined and the render calls produce background; re-run
+ *   with a larger capacity.
+ */
+#ifndef GSR_H
+#define GSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *gs_stream;   /* == cudaStream_t */
+
+typedef enum {
+    GS_OK = 0,
+    GS_ERR_CONFIG = 1,
+    GS_ERR_RANGE = 2,
+    GS_ERR_CAPACITY = 3,
+    GS_ERR_CUDA = 4,
+    GS_ERR_UNSUPPORTED = 5
+} gs_status;
+
+typedef enum {
+    GS_PINHOLE = 0,               /* PAPER.md:96-100, Eq. 3                        */
+    GS_FISHEYE_EQUIDISTANT = 1,   /* BASELINE Fisheye config; replaces Eq. 4 (DESIGN R4) */
+    GS_LIDAR_SPINNING = 2         /* PAPER.md:108-114, Eq. 5                       */
+} gs_sensor_kind;
+
+#define GS_MAX_BEAMS 256
+
+/* Surfel attributes {mu, R, S, rho, r, alpha} after decoding.
+ * All device pointers, fp32, contiguous row-major, read-only. */
+typedef struct {
+    int64_t n;                   /* number of surfels, >= 0 (0 renders background)    */
+    const float *means;          /* [n,3] world metres                                 */
+    const float *quats;          /* [n,4] (w,x,y,z); normalised inside                 */
+    const float *scales;         /* [n,2] s_u, s_v > 0 (linear)                         */
+    const float *opacities;      /* [n] in [0,1] (post-sigmoid)                         */
+    const float *sh;             /* [n,(d+1)^2,3] SH coefficients; cameras only         */
+    int32_t sh_degree;           /* d in 0..3                                           */
+    const float *intensity;      /* [n] LiDAR intensity r in [0,1]; LiDAR only          */
+    const float *raydrop_logit;  /* [n] LiDAR ray-drop logit (p = sigmoid); LiDAR only  */
+} gs_surfels;
+
+/* Sensor model.  world_to_sensor = [R|t] row-major 3x4:
+ * p_sensor = R p_world + t.  Camera frame x right, y down, z forward; LiDAR
+ * frame x forward, y left, z up. */
+typedef struct {
+    int32_t kind;                /* gs_sensor_kind                                      */
+    int32_t width, height;       /* pixels; LiDAR: width = azimuth columns, height = beams */
+    float world_to_sensor[12];
+    float fx, fy, cx, cy;        /* cameras: pixel (i,j) samples (i+1/2, j+1/2)         */
+    float k[4];                  /* fisheye Kannala-Brandt k1..k4 (theta_d polynomial)  */
+    float theta_max;             /* fisheye half field of view (rad), in (0, pi)       */
+    const float *beam_elevation; /* LiDAR [height] elevations (rad), strictly decreasing, HOST */
+    float azimuth0, azimuth_step;/* LiDAR column j has azimuth azimuth0 + j*azimuth_step */
+} gs_sensor;
+
+/* Compositing constants (north_star); gs_default_opts() fills the defaults. */
+typedef struct {
+    int32_t tile_w, tile_h;      /* 16, 16 (camera) -- tile_w*tile_h threads per CTA     */
+    float near_plane;            /* 0.2 m                                               */
+    float alpha_max;             /* 0.99                                                */
+    float alpha_min;             /* 1/255                                               */
+    float t_min;                 /* 1e-4 (0 disables early termination)                 */
+    float support_rho;           /* 9 (3-sigma support, rho = u^2+v^2)                  */
+    float lowpass_sigma_px;      /* 1/sqrt(2) px (cameras)                              */
+    float bg_rgb[3];             /* 0,0,0                                               */
+    float bg_range;              /* 0                                                   */
+    float bg_raydrop;            /* 1                                                   */
+} gs_opts;
+
+void gs_default_opts(gs_opts *opts);
+
+/* Bytes of the per-surfel projection buffer for n surfels of this sensor
+ * kind (records, tile rects, depth keys, counts, compaction lists, header). */
+size_t gs_projected_bytes(int64_t n, int32_t kind);
+
+/* Bytes of gs_bin_sort's workspace for n surfels and pair_capacity pairs. */
+size_t gs_sort_workspace_bytes(int64_t n, int64_t pair_capacity, const gs_sensor *sensor,
+                               const gs_opts *opts);
+
+/* Number of tiles of the sensor's image under opts (tile_ranges has 2 u32
+ * per tile). */
+int64_t gs_num_tiles(const gs_sensor *sensor, const gs_opts *opts);
+
+/*
+ * gs_project -- per-surfel projection (Eq. 1; SH colour and
+ * low-pass bound; attributes P:78).  For every surfel: the
+ * sensor-frame local-to-sensor map of Eq. 1 in its intersection form, the
+ * projected centre, the fp32 depth key (DESIGN reading R9), the oriented
+ * normal, the SH colour (cameras) or intensity / ray-drop probability
+ * (LiDAR), and a conservative 3-sigma bound as a rectangle of tiles.
+ * Then compacts the visible surfels and counts the (tile, surfel) pairs.
+ *   projected       device buffer of >= gs_projected_bytes(n, kind) bytes (out)
+ *   d_num_pairs     device int64 (out): total number of pairs P
+ */
+gs_status gs_project(const gs_surfels *surfels, const gs_sensor *sensor, const gs_opts *opts,
+                     void *projected, size_t projected_bytes, int64_t *d_num_pairs,
+                     gs_stream stream);
+
+/*
+ * gs_bin_sort -- tile binning: a stable LSD radix sort of the 64-bit
+ * (tile << 32 | depth-key bits) pair keys (ties by surfel index), then tile
+ * ranges.  The 32 depth bits are sorted once per visible surfel before the
+ * pairs are emitted (an LSD sort may do its low digits on any order-preserving
+ * expansion); the tile digits are then sorted over the P pairs.
+ *   projected       buffer written by gs_project for the same surfels/sensor/opts
+ *   keys            device [pair_capacity] u64 (out, may be NULL): sorted keys
+ *   values          device [pair_capacity] u32 (out): surfel index of each sorted pair
+ *   tile_ranges     device [num_tiles, 2] u32 (out): [start, end) into values per tile
+ *   workspace       device scratch of >= gs_sort_workspace_bytes() bytes
+ *   d_overflow      device int32 (out): 1 if P > pair_capacity, else 0
+ */
+gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sensor *sensor,
+                      const gs_opts *opts, uint64_t *keys, uint32_t *values,
+                      int64_t pair_capacity, uint32_t *tile_ranges, void *workspace,
+                      size_t workspace_bytes, int32_t *d_overflow, gs_stream stream);
+
+/*
+ * gs_render_camera -- front-to-back compositing for pinhole and equidistant
+ * fisheye cameras: per pixel, exact ray-splat intersection (Eq. 2)
+ * with the unified plane pair (Eq. 3 / R4), low-pass floor, alpha =
+ * min(alpha_max, o G), skip alpha < alpha_min, stop before T < t_min.
+ * Outputs planar fp32 (any may be NULL except alpha):
+ *   rgb [3,H,W], depth [H,W] (normalised expected depth, 0 where alpha = 0),
+ *   normal [3,H,W] (sensor frame, unnormalised composite), alpha [H,W].
+ * d_overflow (may be NULL) is gs_bin_sort's flag: if set, outputs are background.
+ */
+gs_status gs_render_camera(const void *projected, int64_t n, const uint32_t *values,
+                           const uint32_t *tile_ranges, const int32_t *d_overflow,
+                           const gs_sensor *sensor, const gs_opts *opts, float *rgb,
+                           float *depth, float *normal, float *alpha, gs_stream stream);
+
+/*
+ * gs_render_lidar -- range-image compositing (Eq. 5; ray-drop and
+ * intensity).  Outputs planar fp32 [H,W] each (any may be NULL
+ * except alpha): range (0 = no return), intensity, raydrop probability
+ * (composited with background 1), alpha.
+ */
+gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *values,
+                          const uint32_t *tile_ranges, const int32_t *d_overflow,
+                          const gs_sensor *sensor, const gs_opts *opts, float *range,
+                          float *intensity, float *raydrop, float *alpha, gs_stream stream);
+
+const char *gs_status_string(gs_status status);
+const char *gs_last_error(void);
+
+/* Bytes of one projected surfel record for this sensor kind (debug/tests). */
+int32_t gs_record_bytes(int32_t kind);
+
+/* Byte offsets inside the projected buffer (debug/tests): offs[0] records
+ * [n, gs_record_bytes], offs[1] tile rects [n] int16x4 (x0,y0,x1,y1; x1 may
+ * exceed the tile columns for LiDAR azimuth wrap), offs[2] depth keys [n] u32
+ * (fp32 bits; 0xffffffff if culled), offs[3] pair counts [n] u32, offs[4]
+ * total bytes.  The header at offset 0 holds u32 n_visible at +0 and int64
+ * num_pairs at +8. */
+void gs_projected_offsets(int64_t n, int32_t kind, size_t offs[5]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSR_H */

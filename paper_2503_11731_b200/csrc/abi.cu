@@ -1,0 +1,261 @@
+// abi.cu -- the C-ABI of include/gsr.h: host-side validation, parameter
+// packing and launches.  Stateless: no allocation, no globals besides the
+// thread-local error message.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "gsr_internal.cuh"
+
+namespace gsr {
+cudaError_t launch_project(const DevSurfels &, const DevSensor &, const DevOpts &, void *, int64_t *,
+                           cudaStream_t);
+size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles);
+cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
+                            uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
+                            int32_t *d_overflow, cudaStream_t st);
+cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
+                                 const int32_t *, const DevSensor &, const DevOpts &, float *, float *,
+                                 float *, float *, cudaStream_t);
+cudaError_t launch_render_lidar(const void *, int64_t, const uint32_t *, const uint32_t *,
+                                const int32_t *, const DevSensor &, const DevOpts &, float *, float *,
+                                float *, float *, cudaStream_t);
+}  // namespace gsr
+
+using namespace gsr;
+
+static thread_local char g_err[512];
+
+static gs_status fail(gs_status s, const char *fmt, const char *arg = "") {
+    snprintf(g_err, sizeof(g_err), fmt, arg);
+    return s;
+}
+static gs_status cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return GS_ERR_CUDA;
+}
+
+extern "C" void gs_default_opts(gs_opts *o) {
+    if (!o) return;
+    o->tile_w = 16;
+    o->tile_h = 16;
+    o->near_plane = 0.2f;
+    o->alpha_max = 0.99f;
+    o->alpha_min = 1.0f / 255.0f;
+    o->t_min = 1e-4f;
+    o->support_rho = 9.0f;
+    o->lowpass_sigma_px = 0.70710678118654752f;
+    o->bg_rgb[0] = o->bg_rgb[1] = o->bg_rgb[2] = 0.f;
+    o->bg_range = 0.f;
+    o->bg_raydrop = 1.f;
+}
+
+extern "C" int32_t gs_record_bytes(int32_t kind) { return record_floats(kind) * 4; }
+
+extern "C" size_t gs_projected_bytes(int64_t n, int32_t kind) { return ProjLayout(n, kind).total; }
+
+extern "C" void gs_projected_offsets(int64_t n, int32_t kind, size_t offs[5]) {
+    const ProjLayout L(n, kind);
+    offs[0] = L.rec;
+    offs[1] = L.rect;
+    offs[2] = L.key;
+    offs[3] = L.cnt;
+    offs[4] = L.total;
+}
+
+static gs_status check_opts(const gs_opts *o) {
+    if (!o) return fail(GS_ERR_CONFIG, "opts is NULL");
+    if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 1024)
+        return fail(GS_ERR_RANGE, "tile shape must give 1..1024 threads per CTA");
+    if (!(o->near_plane > 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max <= 1.f) ||
+        !(o->alpha_min >= 0.f) || !(o->t_min >= 0.f) || !(o->support_rho > 0.f) ||
+        !(o->lowpass_sigma_px > 0.f))
+        return fail(GS_ERR_RANGE, "compositing constants out of range");
+    return GS_OK;
+}
+
+static gs_status check_sensor(const gs_sensor *s) {
+    if (!s) return fail(GS_ERR_CONFIG, "sensor is NULL");
+    if (s->kind < 0 || s->kind > 2) return fail(GS_ERR_CONFIG, "unknown sensor kind");
+    if (s->width < 1 || s->height < 1) return fail(GS_ERR_CONFIG, "width/height < 1");
+    if (s->width > 32767 * 8 || s->height > 32767 * 8) return fail(GS_ERR_RANGE, "image too large");
+    if (s->kind != GS_LIDAR_SPINNING) {
+        if (!(s->fx > 0.f) || !(s->fy > 0.f)) return fail(GS_ERR_RANGE, "focal length must be > 0");
+        if (s->kind == GS_FISHEYE_EQUIDISTANT && !(s->theta_max > 0.f && s->theta_max < (float)M_PI))
+            return fail(GS_ERR_RANGE, "theta_max outside (0, pi)");
+    } else {
+        if (!s->beam_elevation) return fail(GS_ERR_CONFIG, "beam_elevation is NULL");
+        if (s->height > GS_MAX_BEAMS) return fail(GS_ERR_RANGE, "more than GS_MAX_BEAMS beams");
+        for (int r = 1; r < s->height; ++r)
+            if (!(s->beam_elevation[r] < s->beam_elevation[r - 1]))
+                return fail(GS_ERR_RANGE, "beam elevations must be strictly decreasing");
+        const double span = (double)s->width * (double)s->azimuth_step;
+        if (!(s->azimuth_step > 0.f) || !(span <= 2.0 * M_PI * (1.0 + 1e-6)))
+            return fail(GS_ERR_RANGE, "azimuth span outside (0, 2pi]");
+    }
+    return GS_OK;
+}
+
+static DevSensor make_dev_sensor(const gs_sensor *s, const gs_opts *o) {
+    DevSensor d;
+    memset(&d, 0, sizeof(d));
+    d.kind = s->kind;
+    d.width = s->width;
+    d.height = s->height;
+    d.tw = o->tile_w;
+    d.th = o->tile_h;
+    d.ntx = (s->width + o->tile_w - 1) / o->tile_w;
+    d.nty = (s->height + o->tile_h - 1) / o->tile_h;
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) d.R[3 * r + c] = s->world_to_sensor[4 * r + c];
+        d.t[r] = s->world_to_sensor[4 * r + 3];
+    }
+    for (int c = 0; c < 3; ++c) {   // origin o = -R^T t (fp64, rounded once)
+        double acc = 0.0;
+        for (int r = 0; r < 3; ++r) acc -= (double)d.R[3 * r + c] * (double)d.t[r];
+        d.ow[c] = (float)acc;
+    }
+    d.fx = s->fx; d.fy = s->fy; d.cx = s->cx; d.cy = s->cy;
+    for (int k = 0; k < 4; ++k) d.k[k] = s->k[k];
+    d.theta_max = s->theta_max;
+    {
+        const double th = s->theta_max, t2 = th * th;
+        d.tdmax = th * (1.0 + (double)s->k[0] * t2 + (double)s->k[1] * t2 * t2 +
+                        (double)s->k[2] * t2 * t2 * t2 + (double)s->k[3] * t2 * t2 * t2 * t2);
+    }
+    d.az0 = s->azimuth0;
+    d.az_step = s->azimuth_step;
+    if (s->kind == GS_LIDAR_SPINNING) {
+        d.nbeams = s->height;
+        for (int r = 0; r < s->height; ++r) d.beam[r] = s->beam_elevation[r];
+        d.full_turn = fabs((double)s->width * (double)s->azimuth_step - 2.0 * M_PI) < 1e-5;
+    }
+    return d;
+}
+
+static DevOpts make_dev_opts(const gs_opts *o) {
+    DevOpts d;
+    d.near_plane = o->near_plane;
+    d.alpha_max = o->alpha_max;
+    d.alpha_min = o->alpha_min;
+    d.t_min = o->t_min;
+    d.support = o->support_rho;
+    d.sigma2 = o->lowpass_sigma_px * o->lowpass_sigma_px;
+    d.inv_sigma2 = 1.0f / d.sigma2;
+    for (int c = 0; c < 3; ++c) d.bg[c] = o->bg_rgb[c];
+    d.bg_range = o->bg_range;
+    d.bg_raydrop = o->bg_raydrop;
+    return d;
+}
+
+extern "C" int64_t gs_num_tiles(const gs_sensor *s, const gs_opts *o) {
+    if (check_sensor(s) != GS_OK || check_opts(o) != GS_OK) return -1;
+    return (int64_t)((s->width + o->tile_w - 1) / o->tile_w) * ((s->height + o->tile_h - 1) / o->tile_h);
+}
+
+extern "C" size_t gs_sort_workspace_bytes(int64_t n, int64_t cap, const gs_sensor *s, const gs_opts *o) {
+    const int64_t nt = gs_num_tiles(s, o);
+    if (nt < 0) return 0;
+    return sort_workspace_bytes(n, cap, nt);
+}
+
+extern "C" gs_status gs_project(const gs_surfels *sf, const gs_sensor *s, const gs_opts *o, void *projected,
+                                size_t projected_bytes, int64_t *d_num_pairs, gs_stream stream) {
+    gs_status st;
+    if ((st = check_sensor(s)) != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if (!sf) return fail(GS_ERR_CONFIG, "surfels is NULL");
+    if (sf->n < 0 || sf->n >= (1ll << 30)) return fail(GS_ERR_RANGE, "surfel count outside [0, 2^30)");
+    if (!projected) return fail(GS_ERR_CONFIG, "projected is NULL");
+    if (projected_bytes < gs_projected_bytes(sf->n, s->kind))
+        return fail(GS_ERR_CONFIG, "projected buffer too small");
+    if (sf->n > 0) {
+        if (!sf->means || !sf->quats || !sf->scales || !sf->opacities)
+            return fail(GS_ERR_CONFIG, "null surfel attribute pointer");
+        if (s->kind != GS_LIDAR_SPINNING) {
+            if (!sf->sh) return fail(GS_ERR_CONFIG, "cameras need SH coefficients");
+            if (sf->sh_degree < 0 || sf->sh_degree > 3) return fail(GS_ERR_CONFIG, "sh_degree outside 0..3");
+        }
+        if (((uintptr_t)sf->quats & 15) != 0) return fail(GS_ERR_CONFIG, "quats must be 16-byte aligned");
+    }
+    if (((uintptr_t)projected & 255) != 0) return fail(GS_ERR_CONFIG, "projected must be 256-byte aligned");
+    DevSurfels ds;
+    ds.n = sf->n;
+    ds.means = sf->means; ds.quats = sf->quats; ds.scales = sf->scales; ds.opac = sf->opacities;
+    ds.sh = sf->sh; ds.inten = sf->intensity; ds.drop = sf->raydrop_logit;
+    ds.sh_degree = sf->sh_degree;
+    const DevSensor se = make_dev_sensor(s, o);
+    const DevOpts op = make_dev_opts(o);
+    cudaError_t e = launch_project(ds, se, op, projected, d_num_pairs, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_project");
+    return GS_OK;
+}
+
+extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sensor *s, const gs_opts *o,
+                                 uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *tile_ranges,
+                                 void *workspace, size_t workspace_bytes, int32_t *d_overflow,
+                                 gs_stream stream) {
+    gs_status st;
+    if ((st = check_sensor(s)) != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if (n < 0 || n >= (1ll << 30)) return fail(GS_ERR_RANGE, "surfel count outside [0, 2^30)");
+    if (cap < 0 || cap >= (1ll << 30)) return fail(GS_ERR_RANGE, "pair capacity outside [0, 2^30)");
+    if (!projected || !tile_ranges || !d_overflow || !workspace || (cap > 0 && !values))
+        return fail(GS_ERR_CONFIG, "null buffer");
+    const int64_t nt = gs_num_tiles(s, o);
+    if (nt >= (1ll << 24)) return fail(GS_ERR_RANGE, "too many tiles");
+    if (workspace_bytes < sort_workspace_bytes(n, cap, nt)) return fail(GS_ERR_CONFIG, "workspace too small");
+    const int ntx = (s->width + o->tile_w - 1) / o->tile_w;
+    cudaError_t e = launch_bin_sort(projected, n, s->kind, ntx, nt, keys, values, cap, tile_ranges, workspace,
+                                    d_overflow, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_bin_sort");
+    return GS_OK;
+}
+
+extern "C" gs_status gs_render_camera(const void *projected, int64_t n, const uint32_t *values,
+                                      const uint32_t *tile_ranges, const int32_t *d_overflow,
+                                      const gs_sensor *s, const gs_opts *o, float *rgb, float *depth,
+                                      float *normal, float *alpha, gs_stream stream) {
+    gs_status st;
+    if ((st = check_sensor(s)) != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if (s->kind == GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_camera called with a LiDAR sensor");
+    if (!projected || !tile_ranges || !alpha) return fail(GS_ERR_CONFIG, "null buffer");
+    const DevSensor se = make_dev_sensor(s, o);
+    const DevOpts op = make_dev_opts(o);
+    cudaError_t e = launch_render_camera(projected, n, values, tile_ranges, d_overflow, se, op, rgb, depth, normal,
+                                         alpha, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_render_camera");
+    return GS_OK;
+}
+
+extern "C" gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *values,
+                                     const uint32_t *tile_ranges, const int32_t *d_overflow,
+                                     const gs_sensor *s, const gs_opts *o, float *range, float *intensity,
+                                     float *raydrop, float *alpha, gs_stream stream) {
+    gs_status st;
+    if ((st = check_sensor(s)) != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if (s->kind != GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_lidar called with a camera sensor");
+    if (!projected || !tile_ranges || !alpha) return fail(GS_ERR_CONFIG, "null buffer");
+    const DevSensor se = make_dev_sensor(s, o);
+    const DevOpts op = make_dev_opts(o);
+    cudaError_t e = launch_render_lidar(projected, n, values, tile_ranges, d_overflow, se, op, range, intensity,
+                                        raydrop, alpha, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_render_lidar");
+    return GS_OK;
+}
+
+extern "C" const char *gs_status_string(gs_status s) {
+    switch (s) {
+        case GS_OK: return "ok";
+        case GS_ERR_CONFIG: return "configuration error";
+        case GS_ERR_RANGE: return "argument out of range";
+        case GS_ERR_CAPACITY: return "pair capacity exceeded";
+        case GS_ERR_CUDA: return "CUDA error";
+        case GS_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+extern "C" const char *gs_last_error(void) { return g_err; }

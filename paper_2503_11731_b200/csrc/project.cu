@@ -1,0 +1,556 @@
+// project.cu -- gs_project kernels: per-surfel projection (Eq. 1,
+// P:81-89; SH colour and low-pass bound; attributes) and the
+// visible-surfel compaction / pair count (single-pass look-back scan).
+//
+// One thread per surfel.  Quantities whose rounding the compositing kernels
+// would amplify (sensor-frame centre, projected centre, centre direction,
+// intersection rows) are formed in fp64 and rounded once (hi+lo where the
+// kernels need more than fp32), so that the per-pair fp32 arithmetic only
+// sees well-conditioned, centre-relative values.
+#include <math.h>
+
+#include "gsr_internal.cuh"
+#include "scan.cuh"
+
+namespace gsr {
+
+// ------------------------------------------------------------------ helpers
+// Pinned-order sensor-frame coordinate (DESIGN reading R9): every operation
+// an IEEE-rounded fp64 op on exactly promoted fp32 values, no contraction.
+__device__ __forceinline__ double pinned_row(const float *Rr, float tk, float mx, float my,
+                                             float mz) {
+    const double a = __dmul_rn((double)Rr[0], (double)mx);
+    const double b = __dmul_rn((double)Rr[1], (double)my);
+    const double c = __dmul_rn((double)Rr[2], (double)mz);
+    return __dadd_rn(__dadd_rn(__dadd_rn(a, b), c), (double)tk);
+}
+
+struct Box {
+    double x0, x1, y0, y1;
+    __device__ void init() { x0 = y0 = 1e300; x1 = y1 = -1e300; }
+    __device__ void add(double x, double y) {
+        x0 = fmin(x0, x); x1 = fmax(x1, x);
+        y0 = fmin(y0, y); y1 = fmax(y1, y);
+    }
+};
+
+__device__ __forceinline__ double kb_theta_d(const DevSensor &se, double th) {
+    const double t2 = th * th;
+    return th * (1.0 + t2 * ((double)se.k[0] + t2 * ((double)se.k[1] + t2 * ((double)se.k[2] + t2 * (double)se.k[3]))));
+}
+
+// fisheye projection of a sensor-frame point (equidistant Kannala-Brandt)
+__device__ __forceinline__ void fisheye_project(const DevSensor &se, const double m[3], double &px,
+                                                double &py) {
+    const double rxy = sqrt(m[0] * m[0] + m[1] * m[1]);
+    const double th = atan2(rxy, m[2]);
+    const double td = kb_theta_d(se, th);
+    if (rxy > 0.0) {
+        px = (double)se.cx + (double)se.fx * td * m[0] / rxy;
+        py = (double)se.cy + (double)se.fy * td * m[1] / rxy;
+    } else {
+        px = se.cx;
+        py = se.cy;
+    }
+}
+
+// Pixel-space bound of the pinhole 3-sigma disk clipped to z >= near:
+// extremes of the linear-fractional x = X/Z over {u^2+v^2 <= R^2, Z >= near}
+// lie at the circle's stationary points (A c + B s + C = 0) or at the ends of
+// the chord Z = near.
+__device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const double mu[3],
+                                   const double a[3], const double b[3], Box &box) {
+    auto add_pt = [&](double c, double s) {
+        const double X = mu[0] + c * a[0] + s * b[0];
+        const double Y = mu[1] + c * a[1] + s * b[1];
+        const double Z = mu[2] + c * a[2] + s * b[2];
+        if (Z >= nearp * (1.0 - 1e-9)) {
+            const double zz = fmax(Z, nearp * (1.0 - 1e-9));
+            box.add((double)se.fx * X / zz + (double)se.cx, (double)se.fy * Y / zz + (double)se.cy);
+        }
+    };
+    auto solve = [&](double A, double B, double C, bool strict) {
+        const double rr = A * A + B * B;
+        if (!(rr > 0.0)) return;
+        double disc = rr - C * C;
+        if (strict && !(disc > 0.0)) return;
+        disc = sqrt(fmax(disc, 0.0));
+        add_pt((-A * C + B * disc) / rr, (-B * C - A * disc) / rr);
+        add_pt((-A * C - B * disc) / rr, (-B * C + A * disc) / rr);
+    };
+    add_pt(0.0, 0.0);
+    add_pt(1.0, 0.0);
+    for (int ax = 0; ax < 2; ++ax) {
+        const double a0 = mu[ax], a1 = a[ax], a2 = b[ax];
+        const double b0 = mu[2], b1 = a[2], b2 = b[2];
+        solve(a2 * b0 - a0 * b2, a0 * b1 - a1 * b0, a2 * b1 - a1 * b2, false);
+    }
+    solve(a[2], b[2], mu[2] - nearp, true);   // chord on the near plane
+}
+
+// pixel range [i0,i1] -> tile range; returns false if empty
+__device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw, int th,
+                                             int &tx0, int &ty0, int &tx1, int &ty1) {
+    const double m = 1e-3;
+    double x0 = bx.x0 - m - 1e-6 * fabs(bx.x0), x1 = bx.x1 + m + 1e-6 * fabs(bx.x1);
+    double y0 = bx.y0 - m - 1e-6 * fabs(bx.y0), y1 = bx.y1 + m + 1e-6 * fabs(bx.y1);
+    if (!(x0 <= x1) || !(y0 <= y1)) {   // NaN: whole image (conservative)
+        x0 = y0 = -1e30; x1 = y1 = 1e30;
+    }
+    const double i0 = ceil(x0 - 0.5), i1 = floor(x1 - 0.5);
+    const double j0 = ceil(y0 - 0.5), j1 = floor(y1 - 0.5);
+    const int ci0 = (int)fmax(i0, 0.0), ci1 = (int)fmin(i1, (double)(W - 1));
+    const int cj0 = (int)fmax(j0, 0.0), cj1 = (int)fmin(j1, (double)(H - 1));
+    if (ci0 > ci1 || cj0 > cj1) return false;
+    tx0 = ci0 / tw; tx1 = ci1 / tw; ty0 = cj0 / th; ty1 = cj1 / th;
+    return true;
+}
+
+// SH colour, 3DGS real basis (degree <= 3), evaluated in fp32.
+__device__ __forceinline__ void sh_colour(const float *sh, int deg, float x, float y, float z,
+                                          float rgb[3]) {
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    float b[16];
+    b[0] = C0;
+    int nb = 1;
+    if (deg >= 1) {
+        b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x;
+        nb = 4;
+    }
+    if (deg >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        b[4] = 1.0925484305920792f * x * y;
+        b[5] = -1.0925484305920792f * y * z;
+        b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        b[7] = -1.0925484305920792f * x * z;
+        b[8] = 0.5462742152960396f * (xx - yy);
+        nb = 9;
+        if (deg >= 3) {
+            b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * x * y * z;
+            b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * z * (xx - yy);
+            b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+            nb = 16;
+        }
+    }
+    float r = 0.f, g = 0.f, bl = 0.f;
+    for (int j = 0; j < nb; ++j) {
+        r = fmaf(b[j], __ldg(sh + 3 * j + 0), r);
+        g = fmaf(b[j], __ldg(sh + 3 * j + 1), g);
+        bl = fmaf(b[j], __ldg(sh + 3 * j + 2), bl);
+    }
+    rgb[0] = fmaxf(r + 0.5f, 0.f);
+    rgb[1] = fmaxf(g + 0.5f, 0.f);
+    rgb[2] = fmaxf(bl + 0.5f, 0.f);
+}
+
+__device__ __forceinline__ void cross3(const double a[3], const double b[3], double o[3]) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+__device__ __forceinline__ double dot3(const double a[3], const double b[3]) {
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// LiDAR: rows whose beam elevation lies in [lo, hi] (table strictly decreasing)
+__device__ __forceinline__ bool beam_rows(const DevSensor &se, double lo, double hi, int &r0, int &r1) {
+    // first row with beam <= hi
+    int a = 0, b = se.nbeams;
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        if ((double)se.beam[m] <= hi) b = m; else a = m + 1;
+    }
+    r0 = a;
+    // last row with beam >= lo
+    a = 0; b = se.nbeams;
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        if ((double)se.beam[m] < lo) b = m; else a = m + 1;
+    }
+    r1 = a - 1;
+    return r0 <= r1;
+}
+
+// ------------------------------------------------------------------ projection
+template <int KIND>
+__global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_constant__ DevSensor se,
+                                                 DevOpts op, float *__restrict__ rec,
+                                                 short4 *__restrict__ rect,
+                                                 uint32_t *__restrict__ keys,
+                                                 uint32_t *__restrict__ counts) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s.n) return;
+    const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1),
+                mz = __ldg(s.means + 3 * i + 2);
+    double mu[3];
+    mu[0] = pinned_row(se.R + 0, se.t[0], mx, my, mz);
+    mu[1] = pinned_row(se.R + 3, se.t[1], mx, my, mz);
+    mu[2] = pinned_row(se.R + 6, se.t[2], mx, my, mz);
+    float keyf;
+    if (KIND == GS_PINHOLE) {
+        keyf = (float)mu[2];
+    } else {
+        keyf = (float)__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(mu[0], mu[0]), __dmul_rn(mu[1], mu[1])),
+                                           __dmul_rn(mu[2], mu[2])));
+    }
+    const float o = __ldg(s.opac + i);
+    // opacity-aware support: alpha >= alpha_min needs rho <= 2 ln(o / alpha_min)
+    float rc = op.support;
+    if (op.alpha_min > 0.f) rc = fminf(rc, 2.0f * logf(o / op.alpha_min));
+    const float rcut3 = rc * 1.0001f + 1e-4f;
+    bool vis = (keyf >= op.near_plane) && (rcut3 >= 0.f) && (o > 0.f);
+
+    const float su = __ldg(s.scales + 2 * i), sv = __ldg(s.scales + 2 * i + 1);
+    vis = vis && (su > 0.f) && (sv > 0.f) && isfinite(su) && isfinite(sv);
+    int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+    double A[3], Bv[3], N[3];
+    if (vis) {
+        const float4 qf = __ldg(reinterpret_cast<const float4 *>(s.quats) + i);
+        double qw = qf.x, qx = qf.y, qy = qf.z, qz = qf.w;
+        const double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+        qw /= nq; qx /= nq; qy /= nq; qz /= nq;
+        const double Rq[3][3] = {
+            {1.0 - 2.0 * (qy * qy + qz * qz), 2.0 * (qx * qy - qw * qz), 2.0 * (qx * qz + qw * qy)},
+            {2.0 * (qx * qy + qw * qz), 1.0 - 2.0 * (qx * qx + qz * qz), 2.0 * (qy * qz - qw * qx)},
+            {2.0 * (qx * qz - qw * qy), 2.0 * (qy * qz + qw * qx), 1.0 - 2.0 * (qx * qx + qy * qy)}};
+        for (int r = 0; r < 3; ++r) {
+            const double s0 = se.R[3 * r], s1 = se.R[3 * r + 1], s2 = se.R[3 * r + 2];
+            A[r] = s0 * Rq[0][0] + s1 * Rq[1][0] + s2 * Rq[2][0];
+            Bv[r] = s0 * Rq[0][1] + s1 * Rq[1][1] + s2 * Rq[2][1];
+            N[r] = s0 * Rq[0][2] + s1 * Rq[1][2] + s2 * Rq[2][2];
+        }
+        vis = isfinite(N[0] + N[1] + N[2] + A[0] + Bv[0]);
+    }
+    const double rlp = sqrt((double)rcut3 * (double)op.sigma2);   // low-pass disc radius (px)
+    if (vis) {
+        const double Rr = sqrt((double)rcut3);
+        if (KIND == GS_PINHOLE) {
+            double a[3], b[3];
+            for (int r = 0; r < 3; ++r) { a[r] = Rr * su * A[r]; b[r] = Rr * sv * Bv[r]; }
+            Box bx;
+            bx.init();
+            pinhole_disk_bound(se, (double)op.near_plane, mu, a, b, bx);
+            const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
+            const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
+            bx.add(cx - rlp, cy - rlp);
+            bx.add(cx + rlp, cy + rlp);
+            vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1);
+        } else {
+            const double r = sqrt(dot3(mu, mu));
+            const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
+            const double R3 = Rr * (double)fmaxf(su, sv);
+            const bool whole = !(R3 < 0.999 * r);
+            const double beta = whole ? 0.0 : asin(R3 / r);
+            if (KIND == GS_FISHEYE_EQUIDISTANT) {
+                Box bx;
+                bx.init();
+                const double tm = (double)se.theta_max;
+                if (whole) {
+                    const double rad = kb_theta_d(se, tm);
+                    bx.add(se.cx - se.fx * rad, se.cy - se.fy * rad);
+                    bx.add(se.cx + se.fx * rad, se.cy + se.fy * rad);
+                } else {
+                    const double thc = acos(fmin(1.0, fmax(-1.0, m[2])));
+                    const double thlo = fmax(0.0, thc - beta), thhi = fmin(tm, thc + beta);
+                    if (thlo <= tm) {
+                        const double r0 = kb_theta_d(se, thlo), r1 = kb_theta_d(se, thhi);
+                        bool allpsi = (beta >= thc) || (thc + beta >= M_PI);
+                        double dpsi = M_PI;
+                        if (!allpsi) {
+                            const double sb = sin(beta) / sin(thc);
+                            if (sb >= 1.0) allpsi = true; else dpsi = asin(sb);
+                        }
+                        if (allpsi) {
+                            bx.add(se.cx - se.fx * r1, se.cy - se.fy * r1);
+                            bx.add(se.cx + se.fx * r1, se.cy + se.fy * r1);
+                        } else {
+                            const double psic = atan2(m[1], m[0]);
+                            const double p0 = psic - dpsi, p1 = psic + dpsi;
+                            const double rads[2] = {r0, r1};
+                            for (int k = 0; k < 2; ++k) {
+                                bx.add(se.cx + se.fx * rads[k] * cos(p0), se.cy + se.fy * rads[k] * sin(p0));
+                                bx.add(se.cx + se.fx * rads[k] * cos(p1), se.cy + se.fy * rads[k] * sin(p1));
+                            }
+                            // axis directions inside [p0, p1]
+                            for (int q = -4; q <= 4; ++q) {
+                                const double ang = q * (0.5 * M_PI);
+                                if (ang >= p0 && ang <= p1)
+                                    for (int k = 0; k < 2; ++k)
+                                        bx.add(se.cx + se.fx * rads[k] * cos(ang),
+                                               se.cy + se.fy * rads[k] * sin(ang));
+                            }
+                        }
+                    }
+                }
+                double cxp, cyp;
+                fisheye_project(se, mu, cxp, cyp);
+                bx.add(cxp - rlp, cyp - rlp);
+                bx.add(cxp + rlp, cyp + rlp);
+                vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1);
+            } else {   // LiDAR: angular box with azimuth wrap
+                const int W = se.width;
+                int r0 = 0, r1 = se.nbeams - 1, c0 = 0, c1 = W - 1;
+                bool allaz = whole;
+                if (!whole) {
+                    const double elc = asin(fmin(1.0, fmax(-1.0, m[2])));
+                    const double eps = 1e-6;
+                    vis = beam_rows(se, elc - beta - eps, elc + beta + eps, r0, r1);
+                    if (beta >= 0.5 * M_PI - fabs(elc)) allaz = true;
+                    double daz = M_PI;
+                    if (!allaz) {
+                        const double sb = sin(beta) / cos(elc);
+                        if (sb >= 1.0) allaz = true; else daz = asin(sb);
+                    }
+                    if (!allaz) {
+                        const double azc = atan2(m[1], m[0]);
+                        const double step = (double)se.az_step;
+                        const double ulo = (azc - daz - (double)se.az0) / step;
+                        const double uhi = (azc + daz - (double)se.az0) / step;
+                        double jlo = ceil(ulo) - 1.0, jhi = floor(uhi) + 1.0;
+                        if (se.full_turn) {
+                            if (jhi - jlo + 1.0 >= (double)W) {
+                                allaz = true;
+                            } else {
+                                double k = floor(jlo / (double)W);
+                                jlo -= k * W;
+                                jhi -= k * W;
+                                c0 = (int)jlo;
+                                c1 = (int)jhi;   // may exceed W-1: wraps
+                            }
+                        } else {
+                            // partial turn: union of the shifts by +-2pi, hull
+                            const double per = 2.0 * M_PI / step;
+                            double lo = 1e30, hi = -1e30;
+                            for (int kk = -1; kk <= 1; ++kk) {
+                                const double a0 = fmax(jlo + kk * per, 0.0), a1 = fmin(jhi + kk * per, (double)(W - 1));
+                                if (a0 <= a1) { lo = fmin(lo, a0); hi = fmax(hi, a1); }
+                            }
+                            if (lo > hi) vis = false;
+                            else { c0 = (int)ceil(lo); c1 = (int)floor(hi); if (c0 > c1) vis = false; }
+                        }
+                    }
+                }
+                if (vis) {
+                    const int ntx = se.ntx;
+                    if (allaz) {
+                        tx0 = 0; tx1 = ntx - 1;
+                    } else {
+                        tx0 = c0 / se.tw;
+                        tx1 = c1 < W ? c1 / se.tw : ntx + (c1 - W) / se.tw;
+                        if (tx1 - tx0 + 1 >= ntx) { tx0 = 0; tx1 = ntx - 1; }
+                    }
+                    ty0 = r0 / se.th;
+                    ty1 = r1 / se.th;
+                }
+            }
+        }
+    }
+    if (!vis) {
+        keys[i] = 0xffffffffu;
+        counts[i] = 0;
+        rect[i] = make_short4(0, 0, -1, -1);
+        return;
+    }
+    keys[i] = __float_as_uint(keyf);
+    counts[i] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    rect[i] = make_short4((short)tx0, (short)ty0, (short)tx1, (short)ty1);
+
+    // oriented normal (faces the sensor), attributes
+    const bool flip = dot3(N, mu) > 0.0;
+    const float nsx = (float)(flip ? -N[0] : N[0]), nsy = (float)(flip ? -N[1] : N[1]),
+                nsz = (float)(flip ? -N[2] : N[2]);
+
+    if (KIND == GS_PINHOLE) {
+        float R[PH_FLOATS];
+        // rows of adj([t_u|t_v|mu]) / (s_u s_v) restricted to (dx/fx, dy/fy, 0)
+        double r0[3], r1[3];
+        cross3(Bv, mu, r0);   // (t_v x mu) / s_u
+        cross3(mu, A, r1);    // (mu x t_u) / s_v
+        const double det = dot3(N, mu);
+        const double ifx = 1.0 / (double)se.fx, ify = 1.0 / (double)se.fy;
+        R[PH_A00] = (float)(r0[0] / su * ifx);
+        R[PH_A01] = (float)(r0[1] / su * ify);
+        R[PH_A10] = (float)(r1[0] / sv * ifx);
+        R[PH_A11] = (float)(r1[1] / sv * ify);
+        R[PH_A20] = (float)(N[0] * ifx);
+        R[PH_A21] = (float)(N[1] * ify);
+        R[PH_QC] = (float)(det / mu[2]);
+        R[PH_RCUT3] = rcut3;
+        const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
+        const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
+        split_hilo(cx, R[PH_CHX], R[PH_CLX]);
+        split_hilo(cy, R[PH_CHY], R[PH_CLY]);
+        R[PH_RCUT2] = rcut3 * op.sigma2;
+        R[PH_O] = o;
+        R[PH_DET] = (float)det;
+        R[PH_ZC] = (float)mu[2];
+        const float vx = mx - se.ow[0], vy = my - se.ow[1], vz = mz - se.ow[2];
+        const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
+        const int nc = (s.sh_degree + 1) * (s.sh_degree + 1);
+        float rgb[3];
+        sh_colour(s.sh + (size_t)i * nc * 3, s.sh_degree, vx * vn, vy * vn, vz * vn, rgb);
+        R[PH_R] = rgb[0]; R[PH_G] = rgb[1]; R[PH_B] = rgb[2];
+        R[PH_NX] = nsx; R[PH_NY] = nsy; R[PH_NZ] = nsz;
+        R[22] = 0.f; R[23] = 0.f;
+        float4 *dst = reinterpret_cast<float4 *>(rec + (size_t)i * PH_FLOATS);
+#pragma unroll
+        for (int k = 0; k < PH_FLOATS / 4; ++k)
+            dst[k] = make_float4(R[4 * k], R[4 * k + 1], R[4 * k + 2], R[4 * k + 3]);
+    } else {
+        constexpr int NF = KIND == GS_FISHEYE_EQUIDISTANT ? FE_FLOATS : LI_FLOATS;
+        float R[NF];
+#pragma unroll
+        for (int k = 0; k < NF; ++k) R[k] = 0.f;
+        const double r = sqrt(dot3(mu, mu));
+        const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
+        for (int k = 0; k < 3; ++k) split_hilo(m[k], R[RY_MH + k], R[RY_ML + k]);
+        double u[3], v[3];
+        cross3(Bv, m, u);   // U = r (R t_v x m) / s_u
+        cross3(m, A, v);    // V = r (m x R t_u) / s_v
+        const double det = dot3(N, m);
+        for (int k = 0; k < 3; ++k) {
+            R[RY_U + k] = (float)(r * u[k] / su);
+            R[RY_V + k] = (float)(r * v[k] / sv);
+            R[RY_N + k] = (float)N[k];
+        }
+        R[RY_DET] = (float)det;
+        R[RY_RDET] = (float)(r * det);
+        R[RY_RCUT3] = rcut3;
+        R[RY_O] = o;
+        R[RY_RC] = (float)r;
+        if (KIND == GS_FISHEYE_EQUIDISTANT) {
+            double cxp, cyp;
+            fisheye_project(se, mu, cxp, cyp);
+            split_hilo(cxp, R[FE_CHX], R[FE_CLX]);
+            split_hilo(cyp, R[FE_CHY], R[FE_CLY]);
+            R[FE_RCUT2] = rcut3 * op.sigma2;
+            const float vx = mx - se.ow[0], vy = my - se.ow[1], vz = mz - se.ow[2];
+            const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
+            const int nc = (s.sh_degree + 1) * (s.sh_degree + 1);
+            float rgb[3];
+            sh_colour(s.sh + (size_t)i * nc * 3, s.sh_degree, vx * vn, vy * vn, vz * vn, rgb);
+            R[FE_R] = rgb[0]; R[FE_G] = rgb[1]; R[FE_B] = rgb[2];
+            R[FE_NX] = nsx; R[FE_NY] = nsy; R[FE_NZ] = nsz;
+        } else {
+            R[LI_INT] = s.inten ? __ldg(s.inten + i) : 0.f;
+            const float lg = s.drop ? __ldg(s.drop + i) : 0.f;
+            R[LI_DROP] = (float)(1.0 / (1.0 + exp(-(double)lg)));
+        }
+        float4 *dst = reinterpret_cast<float4 *>(rec + (size_t)i * NF);
+#pragma unroll
+        for (int k = 0; k < NF / 4; ++k)
+            dst[k] = make_float4(R[4 * k], R[4 * k + 1], R[4 * k + 2], R[4 * k + 3]);
+    }
+}
+
+// ------------------------------------------------------------------ compaction
+// Visible surfels (count > 0) in index order -> (vis_key, vis_id); totals of
+// visible surfels and of pairs -> header and d_num_pairs.  One CTA = 2048
+// surfels; each lane owns 8 consecutive surfels; decoupled look-back.
+__global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__restrict__ keys,
+                                                          const uint32_t *__restrict__ counts,
+                                                          int64_t n, uint32_t *__restrict__ vkey,
+                                                          uint32_t *__restrict__ vid,
+                                                          unsigned long long *st_vis,
+                                                          unsigned long long *st_pairs,
+                                                          ProjHeader *hdr, int64_t *d_num_pairs) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_wv[SCAN_THREADS / 32], s_wp[SCAN_THREADS / 32];
+    __shared__ unsigned long long s_excl_v;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->scan_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)(warp * 32 + lane) * SCAN_ITEMS;
+    uint32_t c[SCAN_ITEMS];
+    uint32_t lv = 0, lp = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t idx = base + j;
+        c[j] = idx < n ? counts[idx] : 0u;
+        lv += c[j] > 0 ? 1u : 0u;
+        lp += c[j];
+    }
+    // warp scans (inclusive) of per-lane totals
+    unsigned long long iv = warp_inclusive_scan<unsigned long long>(lv);
+    unsigned long long ip = warp_inclusive_scan<unsigned long long>(lp);
+    if (lane == 31) { s_wv[warp] = iv; s_wp[warp] = ip; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tv = 0, tp = 0;
+        for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+            const unsigned long long a = s_wv[w], b = s_wp[w];
+            s_wv[w] = tv; s_wp[w] = tp;
+            tv += a; tp += b;
+        }
+        const unsigned long long ev = lookback_u64(st_vis, tile, tv);
+        const unsigned long long ep = lookback_u64(st_pairs, tile, tp);
+        s_excl_v = ev;
+        const int64_t end = (int64_t)(tile + 1) * SCAN_TILE;
+        if (end >= n) {   // last tile: totals
+            hdr->n_visible = (uint32_t)(ev + tv);
+            hdr->num_pairs = (int64_t)(ep + tp);
+            if (d_num_pairs) *d_num_pairs = (int64_t)(ep + tp);
+        }
+    }
+    __syncthreads();
+    unsigned long long pos = s_excl_v + s_wv[warp] + iv - lv;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t idx = base + j;
+        if (c[j] > 0) {
+            vkey[pos] = keys[idx];
+            vid[pos] = (uint32_t)idx;
+            ++pos;
+        }
+    }
+}
+
+template __global__ void k_project<GS_PINHOLE>(DevSurfels, const __grid_constant__ DevSensor, DevOpts,
+                                               float *, short4 *, uint32_t *, uint32_t *);
+template __global__ void k_project<GS_FISHEYE_EQUIDISTANT>(DevSurfels, const __grid_constant__ DevSensor,
+                                                           DevOpts, float *, short4 *, uint32_t *,
+                                                           uint32_t *);
+template __global__ void k_project<GS_LIDAR_SPINNING>(DevSurfels, const __grid_constant__ DevSensor,
+                                                      DevOpts, float *, short4 *, uint32_t *,
+                                                      uint32_t *);
+
+// host-side launchers (called from abi.cu)
+cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOpts &op, void *proj,
+                           int64_t *d_num_pairs, cudaStream_t st) {
+    const ProjLayout L(s.n, se.kind);
+    char *base = (char *)proj;
+    ProjHeader *hdr = (ProjHeader *)base;
+    cudaError_t e = cudaMemsetAsync(hdr, 0, sizeof(ProjHeader), st);
+    if (e != cudaSuccess) return e;
+    const size_t nblk = ((size_t)s.n + SCAN_TILE - 1) / SCAN_TILE;
+    e = cudaMemsetAsync(base + L.status, 0, 2 * (nblk + 1) * 8, st);
+    if (e != cudaSuccess) return e;
+    if (s.n == 0) {
+        if (d_num_pairs) return cudaMemsetAsync(d_num_pairs, 0, 8, st);
+        return cudaSuccess;
+    }
+    const unsigned grid = (unsigned)((s.n + 255) / 256);
+    float *rec = (float *)(base + L.rec);
+    short4 *rect = (short4 *)(base + L.rect);
+    uint32_t *key = (uint32_t *)(base + L.key), *cnt = (uint32_t *)(base + L.cnt);
+    if (se.kind == GS_PINHOLE)
+        k_project<GS_PINHOLE><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
+    else if (se.kind == GS_FISHEYE_EQUIDISTANT)
+        k_project<GS_FISHEYE_EQUIDISTANT><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
+    else
+        k_project<GS_LIDAR_SPINNING><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    unsigned long long *stv = (unsigned long long *)(base + L.status);
+    k_compact<<<(unsigned)nblk, SCAN_THREADS, 0, st>>>(key, cnt, s.n, (uint32_t *)(base + L.vkey),
+                                                      (uint32_t *)(base + L.vid), stv, stv + nblk + 1,
+                                                      hdr, d_num_pairs);
+    return cudaGetLastError();
+}
+
+}  // namespace gsr

@@ -1,0 +1,73 @@
+// scan.cuh -- single-pass decoupled look-back primitives (device-wide scans
+// without a host round trip; the element counts live in device memory).
+#pragma once
+#include <stdint.h>
+
+namespace gsr {
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+// 64-bit status word: [63:62] flag (1 = aggregate, 2 = inclusive prefix), [61:0] value.
+constexpr unsigned long long LB_AGG = 1ull << 62;
+constexpr unsigned long long LB_PRE = 2ull << 62;
+constexpr unsigned long long LB_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Publish `aggregate` for tile `tile` and return the exclusive prefix of all
+// earlier tiles.  Called by ONE thread.  Tiles must be numbered in the order
+// their CTAs started (dynamic tile ids), so the spin always terminates.
+__device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *st, uint32_t tile,
+                                                          unsigned long long aggregate) {
+    if (tile == 0) {
+        st_volatile_u64(&st[0], LB_PRE | aggregate);
+        return 0;
+    }
+    st_volatile_u64(&st[tile], LB_AGG | aggregate);
+    unsigned long long excl = 0;
+    int64_t t = (int64_t)tile - 1;
+    while (true) {
+        const unsigned long long s = ld_volatile_u64(&st[t]);
+        const unsigned long long f = s >> 62;
+        if (f == 0) continue;
+        excl += s & LB_VAL;
+        if (f == 2) break;
+        --t;
+    }
+    st_volatile_u64(&st[tile], LB_PRE | (excl + aggregate));
+    return excl;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T x) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(FULL_MASK, x, o);
+        if ((int)lane_id() >= o) x += y;
+    }
+    return x;
+}
+
+}  // namespace gsr

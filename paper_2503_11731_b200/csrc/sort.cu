@@ -1,0 +1,430 @@
+// sort.cu -- gs_bin_sort: tile binning with a stable LSD radix sort of the
+// 64-bit (tile << 32 | depth bits) pair keys (ties by surfel index), and
+// tile-range extraction.  Integer work only; bit-exact by construction.
+//
+// LSD order: the four 8-bit depth digits are sorted first, once per VISIBLE
+// SURFEL (the compacted list of gs_project is in index order, so the sort is
+// stable on the index); pairs are then emitted in that order (which is the
+// order an LSD sort over the emitted pairs would have after its depth
+// digits) and the tile digits are sorted over the pairs.  Every pass is a
+// single "onesweep" kernel: stable in-CTA ranking (warp match_any),
+// decoupled look-back across CTAs for the per-digit offsets, scatter through
+// shared memory.  Element counts are read from device memory, so the whole
+// sequence is free of host synchronisation (CUDA-graph capturable).
+#include <algorithm>
+
+#include "gsr_internal.cuh"
+#include "scan.cuh"
+
+namespace gsr {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // 4096
+constexpr int RS_BINS = 256;
+constexpr uint32_t RS_AGG = 1u << 30, RS_PRE = 2u << 30, RS_VAL = (1u << 30) - 1;
+
+struct SortWs {   // workspace layout of gs_bin_sort
+    size_t misc, hist, dA_k, dA_v, dB_k, dB_v, offs, cstat, tk0, tk1, tv1, dstat, tstat, total;
+    int npass_t;
+    size_t ntile_d, ntile_t, nblk_c;
+};
+
+__host__ __device__ inline int tile_bits_for(int64_t ntiles) {
+    int b = 0;
+    while ((1ll << b) < ntiles) ++b;
+    return b < 1 ? 1 : b;
+}
+
+SortWs sort_layout(int64_t n, int64_t cap, int64_t ntiles) {
+    SortWs w;
+    const size_t N = (size_t)(n > 0 ? n : 0), P = (size_t)(cap > 0 ? cap : 0);
+    const int tb = tile_bits_for(ntiles);
+    w.npass_t = (tb + 7) / 8;
+    w.ntile_d = (N + RS_TILE - 1) / RS_TILE;
+    w.ntile_t = (P + RS_TILE - 1) / RS_TILE;
+    w.nblk_c = (N + SCAN_TILE - 1) / SCAN_TILE;
+    size_t o = 0;
+    w.misc = o; o += 256;                                  // counters
+    w.hist = o; o += align256(8 * RS_BINS * 4);            // [pass][bin] histogram -> bases
+    w.dA_k = o; o += align256(N * 4);
+    w.dA_v = o; o += align256(N * 4);
+    w.dB_k = o; o += align256(N * 4);
+    w.dB_v = o; o += align256(N * 4);
+    w.offs = o; o += align256(N * 4);
+    w.cstat = o; o += align256((w.nblk_c + 1) * 8);
+    w.tk0 = o; o += align256(P * 4);
+    w.tk1 = o; o += align256(P * 4);
+    w.tv1 = o; o += align256(P * 4);
+    w.dstat = o; o += align256(4 * w.ntile_d * RS_BINS * 4);
+    w.tstat = o; o += align256((size_t)w.npass_t * w.ntile_t * RS_BINS * 4);
+    w.total = o;
+    return w;
+}
+
+struct SortMisc {          // at workspace + misc (zeroed per call)
+    uint32_t counter[8];   // dynamic tile ids per radix pass
+    uint32_t scan_counter;
+    uint32_t n_pairs32;    // P (if it fits the capacity)
+    uint32_t pad[54];
+};
+static_assert(sizeof(SortMisc) == 256, "misc");
+
+// ------------------------------------------------------------------ histograms
+// Digit histograms of all passes in one read of the keys.
+__global__ void __launch_bounds__(256) k_hist(const uint32_t *__restrict__ keys, const uint32_t *d_n,
+                                              int npass, int total_bits, uint32_t *__restrict__ ghist,
+                                              const int32_t *d_overflow) {
+    __shared__ uint32_t h[4][RS_BINS];
+    if (d_overflow && *d_overflow) return;
+    for (int i = threadIdx.x; i < 4 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t n = *d_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        for (int p = 0; p < npass; ++p) {
+            const int bits = min(8, total_bits - 8 * p);
+            atomicAdd(&h[p][(k >> (8 * p)) & ((1u << bits) - 1)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; ++p)
+        for (int b = threadIdx.x; b < RS_BINS; b += blockDim.x)
+            if (h[p][b]) atomicAdd(&ghist[p * RS_BINS + b], h[p][b]);
+}
+
+// exclusive scan of each pass's histogram (in place) -> global digit bases
+__global__ void k_hist_scan(uint32_t *ghist, int npass, const int32_t *d_overflow) {
+    __shared__ uint32_t s[RS_BINS];
+    if (d_overflow && *d_overflow) return;
+    for (int p = 0; p < npass; ++p) {
+        const uint32_t v = ghist[p * RS_BINS + threadIdx.x];
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < RS_BINS; o <<= 1) {
+            const uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+            __syncthreads();
+            s[threadIdx.x] += t;
+            __syncthreads();
+        }
+        ghist[p * RS_BINS + threadIdx.x] = s[threadIdx.x] - v;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ onesweep pass
+__global__ void __launch_bounds__(RS_THREADS) k_onesweep(
+    const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, const uint32_t *d_n, int shift, int bits,
+    const uint32_t *__restrict__ gbase, uint32_t *status, uint32_t *counter,
+    const int32_t *d_overflow) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t whist[RS_WARPS][RS_BINS];
+    __shared__ uint32_t tile_excl[RS_BINS];
+    __shared__ uint32_t glob[RS_BINS];
+    __shared__ uint32_t skey[RS_TILE];
+    __shared__ uint32_t sval[RS_TILE];
+    if (d_overflow && *d_overflow) return;
+    const uint32_t n = *d_n;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    for (int i = tid; i < RS_WARPS * RS_BINS; i += RS_THREADS) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t t0 = tile * RS_TILE;
+    if (t0 >= n) return;
+    const uint32_t mask = (1u << bits) - 1;
+    const uint32_t wbase = t0 + warp * (32 * RS_ITEMS);
+    uint32_t k[RS_ITEMS], v[RS_ITEMS], rk[RS_ITEMS];
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint32_t idx = wbase + j * 32 + lane;
+        const bool ok = idx < n;
+        k[j] = ok ? kin[idx] : 0xffffffffu;
+        v[j] = ok ? vin[idx] : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint32_t idx = wbase + j * 32 + lane;
+        const bool ok = idx < n;
+        const uint32_t d = (k[j] >> shift) & mask;
+        const uint32_t peers = __match_any_sync(FULL_MASK, ok ? d : 0x10000u);
+        const uint32_t before = __popc(peers & lt);
+        const uint32_t prev = ok ? whist[warp][d] : 0u;
+        __syncwarp();
+        if (ok && before == 0) whist[warp][d] = prev + __popc(peers);
+        __syncwarp();
+        rk[j] = prev + before;
+    }
+    __syncthreads();
+    // per digit: warp-exclusive offsets and tile count
+    const uint32_t dg = tid;   // RS_THREADS == RS_BINS
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+        const uint32_t c = whist[w][dg];
+        whist[w][dg] = cnt;
+        cnt += c;
+    }
+    // decoupled look-back over tiles for this digit
+    uint32_t excl = 0;
+    uint32_t *st = status + (size_t)tile * RS_BINS + dg;
+    if (tile == 0) {
+        st_volatile_u32(st, RS_PRE | cnt);
+    } else {
+        st_volatile_u32(st, RS_AGG | cnt);
+        int64_t t = (int64_t)tile - 1;
+        while (true) {
+            const uint32_t s = ld_volatile_u32(status + (size_t)t * RS_BINS + dg);
+            const uint32_t f = s >> 30;
+            if (f == 0) continue;
+            excl += s & RS_VAL;
+            if (f == 2) break;
+            --t;
+        }
+        st_volatile_u32(st, RS_PRE | (excl + cnt));
+    }
+    glob[dg] = gbase[dg] + excl;
+    // tile-local exclusive scan over digits (block scan of cnt)
+    {
+        uint32_t x = warp_inclusive_scan<uint32_t>(cnt);
+        __shared__ uint32_t wsum[RS_WARPS];
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t y = lane < RS_WARPS ? wsum[lane] : 0u;
+            y = warp_inclusive_scan<uint32_t>(y);
+            if (lane < RS_WARPS) wsum[lane] = y;
+        }
+        __syncthreads();
+        tile_excl[dg] = x - cnt + (warp > 0 ? wsum[warp - 1] : 0u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) {
+        const uint32_t idx = wbase + j * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (k[j] >> shift) & mask;
+            const uint32_t pos = tile_excl[d] + whist[warp][d] + rk[j];
+            skey[pos] = k[j];
+            sval[pos] = v[j];
+        }
+    }
+    __syncthreads();
+    const uint32_t nt = min((uint32_t)RS_TILE, n - t0);
+    for (uint32_t i = tid; i < nt; i += RS_THREADS) {
+        const uint32_t key = skey[i];
+        const uint32_t d = (key >> shift) & mask;
+        const uint32_t dst = glob[d] + (i - tile_excl[d]);
+        kout[dst] = key;
+        vout[dst] = sval[i];
+    }
+}
+
+// ------------------------------------------------------------------ pair offsets
+// Exclusive scan of counts[vid_sorted[i]] over the V visible surfels in depth
+// order -> emission offsets; the last CTA checks the pair capacity.
+__global__ void __launch_bounds__(SCAN_THREADS) k_pair_offsets(
+    const uint32_t *__restrict__ sid, const uint32_t *__restrict__ counts, const ProjHeader *hdr,
+    uint32_t *__restrict__ offs, unsigned long long *st, SortMisc *misc, int64_t cap,
+    int32_t *d_overflow) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_w[SCAN_THREADS / 32], s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&misc->scan_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t n = hdr->n_visible;
+    if ((int64_t)tile * SCAN_TILE >= (int64_t)n && tile > 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)(warp * 32 + lane) * SCAN_ITEMS;
+    uint32_t c[SCAN_ITEMS];
+    unsigned long long l = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t idx = base + j;
+        c[j] = idx < n ? counts[sid[idx]] : 0u;
+        l += c[j];
+    }
+    const unsigned long long inc = warp_inclusive_scan<unsigned long long>(l);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+            const unsigned long long a = s_w[w];
+            s_w[w] = tot;
+            tot += a;
+        }
+        const unsigned long long e = lookback_u64(st, tile, tot);
+        s_excl = e;
+        if ((int64_t)(tile + 1) * SCAN_TILE >= (int64_t)n) {
+            const unsigned long long P = e + tot;
+            const bool over = (int64_t)P > cap || P >= (1ull << 30);
+            *d_overflow = over ? 1 : 0;
+            misc->n_pairs32 = over ? 0u : (uint32_t)P;
+        }
+    }
+    __syncthreads();
+    unsigned long long pos = s_excl + s_w[warp] + inc - l;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t idx = base + j;
+        if (idx < n) offs[idx] = (uint32_t)pos;
+        pos += c[j];
+    }
+}
+
+// ------------------------------------------------------------------ emission
+// One thread per visible surfel (depth order): its tiles, row-major, at its
+// offset.  Tile ids are reduced modulo ntx (LiDAR azimuth wrap).
+__global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
+                                              const uint32_t *__restrict__ offs,
+                                              const short4 *__restrict__ rect,
+                                              const ProjHeader *hdr, int ntx,
+                                              uint32_t *__restrict__ tkey,
+                                              uint32_t *__restrict__ tval,
+                                              const int32_t *d_overflow) {
+    if (*d_overflow) return;
+    const uint32_t n = hdr->n_visible;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t id = sid[k];
+    uint32_t o = offs[k];
+    const short4 r = rect[id];
+    for (int ty = r.y; ty <= r.w; ++ty)
+        for (int tx = r.x; tx <= r.z; ++tx) {
+            const int t = tx >= ntx ? tx - ntx : tx;
+            tkey[o] = (uint32_t)(ty * ntx + t);
+            tval[o] = id;
+            ++o;
+        }
+}
+
+// ------------------------------------------------------------------ ranges
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tkey, const SortMisc *misc,
+                                                uint32_t *__restrict__ ranges,
+                                                const int32_t *d_overflow) {
+    if (*d_overflow) return;
+    const uint32_t P = misc->n_pairs32;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const uint32_t t = tkey[i];
+    if (i == 0 || tkey[i - 1] != t) ranges[2 * t] = i;
+    if (i == P - 1 || tkey[i + 1] != t) ranges[2 * t + 1] = i + 1;
+}
+
+__global__ void __launch_bounds__(256) k_keys64(const uint32_t *__restrict__ tkey,
+                                                const uint32_t *__restrict__ tval,
+                                                const uint32_t *__restrict__ dkey, const SortMisc *misc,
+                                                unsigned long long *__restrict__ keys,
+                                                const int32_t *d_overflow) {
+    if (*d_overflow) return;
+    const uint32_t P = misc->n_pairs32;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    keys[i] = ((unsigned long long)tkey[i] << 32) | dkey[tval[i]];
+}
+
+// ------------------------------------------------------------------ host
+size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles) {
+    return sort_layout(n, cap, ntiles).total;
+}
+
+cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
+                            uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges,
+                            void *ws, int32_t *d_overflow, cudaStream_t st) {
+    const ProjLayout L(n, kind);
+    const SortWs W = sort_layout(n, cap, ntiles);
+    const char *pb = (const char *)proj;
+    char *wb = (char *)ws;
+    const ProjHeader *hdr = (const ProjHeader *)pb;
+    SortMisc *misc = (SortMisc *)(wb + W.misc);
+    uint32_t *hist = (uint32_t *)(wb + W.hist);
+    cudaError_t e;
+#define CK(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+    CK(cudaMemsetAsync(d_overflow, 0, 4, st));
+    CK(cudaMemsetAsync(wb + W.misc, 0, W.hist + 8 * RS_BINS * 4 - W.misc, st));
+    CK(cudaMemsetAsync(ranges, 0, (size_t)ntiles * 2 * 4, st));
+    CK(cudaMemsetAsync(wb + W.cstat, 0, (W.nblk_c + 1) * 8, st));
+    CK(cudaMemsetAsync(wb + W.dstat, 0, W.total - W.dstat, st));
+    if (n == 0 || cap == 0) {
+        // nothing visible can be binned; flag overflow if pairs exist
+        if (n > 0) {
+            // P > 0 with cap == 0 -> overflow is reported by the offsets kernel
+        } else {
+            return cudaSuccess;
+        }
+    }
+    const uint32_t *d_nvis = &hdr->n_visible;
+    // 1. depth sort of the visible surfels (4 x 8-bit digits)
+    const unsigned hgrid_d = (unsigned)std::min<int64_t>((n + 4095) / 4096, 4 * 148);
+    k_hist<<<hgrid_d > 0 ? hgrid_d : 1, 256, 0, st>>>((const uint32_t *)(pb + L.vkey), d_nvis, 4, 32,
+                                                      hist, nullptr);
+    CK(cudaGetLastError());
+    const uint32_t *ki = (const uint32_t *)(pb + L.vkey), *vi = (const uint32_t *)(pb + L.vid);
+    uint32_t *bufk[2] = {(uint32_t *)(wb + W.dA_k), (uint32_t *)(wb + W.dB_k)};
+    uint32_t *bufv[2] = {(uint32_t *)(wb + W.dA_v), (uint32_t *)(wb + W.dB_v)};
+    // the depth histogram scan and the tile histogram share `hist` rows 0..3 / 4..6
+    k_hist_scan<<<1, RS_BINS, 0, st>>>(hist, 4, nullptr);
+    CK(cudaGetLastError());
+    const unsigned grid_d = (unsigned)(W.ntile_d > 0 ? W.ntile_d : 1);
+    for (int p = 0; p < 4; ++p) {
+        k_onesweep<<<grid_d, RS_THREADS, 0, st>>>(ki, vi, bufk[p & 1], bufv[p & 1], d_nvis, 8 * p, 8,
+                                                  hist + p * RS_BINS,
+                                                  (uint32_t *)(wb + W.dstat) + (size_t)p * W.ntile_d * RS_BINS,
+                                                  &misc->counter[p], nullptr);
+        CK(cudaGetLastError());
+        ki = bufk[p & 1];
+        vi = bufv[p & 1];
+    }
+    // sorted ids now in bufv[1] (after 4 passes), keys in bufk[1]
+    const uint32_t *sid = vi;
+    uint32_t *offs = (uint32_t *)(wb + W.offs);
+    const unsigned gridc = (unsigned)(W.nblk_c > 0 ? W.nblk_c : 1);
+    k_pair_offsets<<<gridc, SCAN_THREADS, 0, st>>>(sid, (const uint32_t *)(pb + L.cnt), hdr, offs,
+                                                   (unsigned long long *)(wb + W.cstat), misc, cap,
+                                                   d_overflow);
+    CK(cudaGetLastError());
+    // 2. emission into the buffer that the tile passes end in `values`
+    const int np = W.npass_t;
+    uint32_t *tk[2] = {(uint32_t *)(wb + W.tk0), (uint32_t *)(wb + W.tk1)};
+    uint32_t *tv[2] = {values, (uint32_t *)(wb + W.tv1)};
+    int cur = np & 1;
+    k_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr,
+                                                         ntx, tk[cur], tv[cur], d_overflow);
+    CK(cudaGetLastError());
+    // 3. tile digits over the pairs
+    const int tb = tile_bits_for(ntiles);
+    const uint32_t *d_np = &misc->n_pairs32;
+    uint32_t *thist = hist + 4 * RS_BINS;
+    const unsigned hgrid_t = (unsigned)std::min<int64_t>((cap + 4095) / 4096, 4 * 148);
+    k_hist<<<hgrid_t > 0 ? hgrid_t : 1, 256, 0, st>>>(tk[cur], d_np, np, tb, thist, d_overflow);
+    CK(cudaGetLastError());
+    k_hist_scan<<<1, RS_BINS, 0, st>>>(thist, np, d_overflow);
+    CK(cudaGetLastError());
+    const unsigned grid_t = (unsigned)(W.ntile_t > 0 ? W.ntile_t : 1);
+    for (int p = 0; p < np; ++p) {
+        const int bits = min(8, tb - 8 * p);
+        k_onesweep<<<grid_t, RS_THREADS, 0, st>>>(tk[cur], tv[cur], tk[cur ^ 1], tv[cur ^ 1], d_np, 8 * p,
+                                                  bits, thist + p * RS_BINS,
+                                                  (uint32_t *)(wb + W.tstat) + (size_t)p * W.ntile_t * RS_BINS,
+                                                  &misc->counter[4 + p], d_overflow);
+        CK(cudaGetLastError());
+        cur ^= 1;
+    }
+    // cur == 0 now: sorted tile keys in tk[0], values in `values`
+    const unsigned gp = (unsigned)((cap + 255) / 256);
+    k_ranges<<<gp > 0 ? gp : 1, 256, 0, st>>>(tk[cur], misc, ranges, d_overflow);
+    CK(cudaGetLastError());
+    if (keys) {
+        k_keys64<<<gp > 0 ? gp : 1, 256, 0, st>>>(tk[cur], values, (const uint32_t *)(pb + L.key), misc,
+                                                  (unsigned long long *)keys, d_overflow);
+        CK(cudaGetLastError());
+    }
+#undef CK
+    return cudaSuccess;
+}
+
+}  // namespace gsr

@@ -1,0 +1,210 @@
+"""ctypes binding of include/gsr.h (argument marshalling only).
+
+Same names as the C-ABI.  Every step of the path runs inside libgsr.so's
+CUDA kernels; this module converts Python objects (torch CUDA tensors,
+scenegen.Sensor-like objects) into the C structs and raises GsError on a
+non-OK status.  There is no CPU fallback: if libgsr.so cannot be loaded the
+import of load() raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+from . import build as _build
+
+GS_OK, GS_ERR_CONFIG, GS_ERR_RANGE, GS_ERR_CAPACITY, GS_ERR_CUDA, GS_ERR_UNSUPPORTED = range(6)
+GS_PINHOLE, GS_FISHEYE_EQUIDISTANT, GS_LIDAR_SPINNING = 0, 1, 2
+GS_MAX_BEAMS = 256
+
+
+class GsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+class gs_surfels(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("quats", C.c_void_p),
+                ("scales", C.c_void_p), ("opacities", C.c_void_p), ("sh", C.c_void_p),
+                ("sh_degree", C.c_int32), ("intensity", C.c_void_p),
+                ("raydrop_logit", C.c_void_p)]
+
+
+class gs_sensor(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("world_to_sensor", C.c_float * 12), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("k", C.c_float * 4),
+                ("theta_max", C.c_float), ("beam_elevation", C.c_void_p),
+                ("azimuth0", C.c_float), ("azimuth_step", C.c_float)]
+
+
+class gs_opts(C.Structure):
+    _fields_ = [("tile_w", C.c_int32), ("tile_h", C.c_int32), ("near_plane", C.c_float),
+                ("alpha_max", C.c_float), ("alpha_min", C.c_float), ("t_min", C.c_float),
+                ("support_rho", C.c_float), ("lowpass_sigma_px", C.c_float),
+                ("bg_rgb", C.c_float * 3), ("bg_range", C.c_float), ("bg_raydrop", C.c_float)]
+
+
+EXPORTS = ["gs_default_opts", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
+           "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
+           "gs_status_string", "gs_last_error", "gs_record_bytes"]
+
+_lib = None
+
+
+def load(build_if_missing: bool = True):
+    """Load libgsr.so (building it in-tree with nvcc if absent or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    so = _build.SO
+    if build_if_missing:
+        so = _build.build()
+    if not os.path.exists(so):
+        raise ImportError(f"libgsr.so not found at {so}; run paper_2503_11731_b200/build.py")
+    lib = C.CDLL(so)
+    P, vp = C.POINTER, C.c_void_p
+    lib.gs_default_opts.argtypes = [P(gs_opts)]
+    lib.gs_default_opts.restype = None
+    lib.gs_projected_bytes.argtypes = [C.c_int64, C.c_int32]
+    lib.gs_projected_bytes.restype = C.c_size_t
+    lib.gs_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, P(gs_sensor), P(gs_opts)]
+    lib.gs_sort_workspace_bytes.restype = C.c_size_t
+    lib.gs_num_tiles.argtypes = [P(gs_sensor), P(gs_opts)]
+    lib.gs_num_tiles.restype = C.c_int64
+    lib.gs_record_bytes.argtypes = [C.c_int32]
+    lib.gs_record_bytes.restype = C.c_int32
+    lib.gs_project.argtypes = [P(gs_surfels), P(gs_sensor), P(gs_opts), vp, C.c_size_t, vp, vp]
+    lib.gs_project.restype = C.c_int
+    lib.gs_bin_sort.argtypes = [vp, C.c_int64, P(gs_sensor), P(gs_opts), vp, vp, C.c_int64, vp, vp,
+                                C.c_size_t, vp, vp]
+    lib.gs_bin_sort.restype = C.c_int
+    lib.gs_render_camera.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp, vp, vp,
+                                     vp, vp]
+    lib.gs_render_camera.restype = C.c_int
+    lib.gs_render_lidar.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp, vp, vp,
+                                    vp, vp]
+    lib.gs_render_lidar.restype = C.c_int
+    lib.gs_projected_offsets.argtypes = [C.c_int64, C.c_int32, vp]
+    lib.gs_projected_offsets.restype = None
+    lib.gs_status_string.argtypes = [C.c_int]
+    lib.gs_status_string.restype = C.c_char_p
+    lib.gs_last_error.argtypes = []
+    lib.gs_last_error.restype = C.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status):
+    if status != GS_OK:
+        lib = load()
+        raise GsError(status, f"{lib.gs_status_string(status).decode()}: {lib.gs_last_error().decode()}")
+
+
+def _ptr(t):
+    """data pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------- struct builders
+def default_opts(**overrides) -> gs_opts:
+    o = gs_opts()
+    load().gs_default_opts(C.byref(o))
+    for k, v in overrides.items():
+        if k == "bg_rgb":
+            o.bg_rgb[:] = [float(x) for x in v]
+        else:
+            setattr(o, k, v)
+    return o
+
+
+class Sensor:
+    """gs_sensor plus the host beam table it points to."""
+
+    def __init__(self, s):
+        self.kind, self.width, self.height = int(s.kind), int(s.width), int(s.height)
+        st = gs_sensor()
+        st.kind, st.width, st.height = self.kind, self.width, self.height
+        st.world_to_sensor[:] = [float(x) for x in np.asarray(s.world_to_sensor, np.float32).ravel()]
+        st.fx, st.fy, st.cx, st.cy = float(s.fx), float(s.fy), float(s.cx), float(s.cy)
+        st.k[:] = [float(x) for x in np.asarray(s.k, np.float32)]
+        st.theta_max = float(s.theta_max)
+        self._beams = None
+        if s.beam_elevation is not None:
+            self._beams = np.ascontiguousarray(s.beam_elevation, np.float32)
+            st.beam_elevation = self._beams.ctypes.data
+        st.azimuth0, st.azimuth_step = float(s.azimuth0), float(s.azimuth_step)
+        self.struct = st
+
+    @property
+    def ref(self):
+        return C.byref(self.struct)
+
+
+def surfels_struct(t: dict) -> gs_surfels:
+    """t: dict of contiguous float32 CUDA tensors (means, quats, scales,
+    opacities[, sh, intensity, raydrop_logit]) and int sh_degree."""
+    s = gs_surfels()
+    s.n = int(t["means"].shape[0])
+    s.means, s.quats, s.scales, s.opacities = (t["means"].data_ptr(), t["quats"].data_ptr(),
+                                               t["scales"].data_ptr(), t["opacities"].data_ptr())
+    s.sh = t["sh"].data_ptr() if t.get("sh") is not None else None
+    s.sh_degree = int(t.get("sh_degree", 0))
+    s.intensity = t["intensity"].data_ptr() if t.get("intensity") is not None else None
+    s.raydrop_logit = t["raydrop_logit"].data_ptr() if t.get("raydrop_logit") is not None else None
+    return s
+
+
+# ---------------------------------------------------------------- the C-ABI, same names
+def gs_projected_bytes(n, kind):
+    return int(load().gs_projected_bytes(int(n), int(kind)))
+
+
+def gs_sort_workspace_bytes(n, cap, sensor: Sensor, opts: gs_opts):
+    return int(load().gs_sort_workspace_bytes(int(n), int(cap), sensor.ref, C.byref(opts)))
+
+
+def gs_num_tiles(sensor: Sensor, opts: gs_opts):
+    return int(load().gs_num_tiles(sensor.ref, C.byref(opts)))
+
+
+def gs_record_bytes(kind):
+    return int(load().gs_record_bytes(int(kind)))
+
+
+def gs_projected_offsets(n, kind):
+    offs = (C.c_size_t * 5)()
+    load().gs_projected_offsets(int(n), int(kind), offs)
+    return dict(rec=offs[0], rect=offs[1], key=offs[2], count=offs[3], total=offs[4])
+
+
+def gs_project(surfels: gs_surfels, sensor: Sensor, opts: gs_opts, projected, d_num_pairs, stream):
+    _check(load().gs_project(C.byref(surfels), sensor.ref, C.byref(opts), _ptr(projected),
+                             projected.numel() * projected.element_size(), _ptr(d_num_pairs),
+                             C.c_void_p(stream)))
+
+
+def gs_bin_sort(projected, n, sensor: Sensor, opts: gs_opts, keys, values, cap, tile_ranges,
+                workspace, d_overflow, stream):
+    _check(load().gs_bin_sort(_ptr(projected), int(n), sensor.ref, C.byref(opts), _ptr(keys),
+                              _ptr(values), int(cap), _ptr(tile_ranges), _ptr(workspace),
+                              workspace.numel() * workspace.element_size(), _ptr(d_overflow),
+                              C.c_void_p(stream)))
+
+
+def gs_render_camera(projected, n, values, tile_ranges, d_overflow, sensor: Sensor, opts: gs_opts,
+                     rgb, depth, normal, alpha, stream):
+    _check(load().gs_render_camera(_ptr(projected), int(n), _ptr(values), _ptr(tile_ranges),
+                                   _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(rgb),
+                                   _ptr(depth), _ptr(normal), _ptr(alpha), C.c_void_p(stream)))
+
+
+def gs_render_lidar(projected, n, values, tile_ranges, d_overflow, sensor: Sensor, opts: gs_opts,
+                    rng, intensity, raydrop, alpha, stream):
+    _check(load().gs_render_lidar(_ptr(projected), int(n), _ptr(values), _ptr(tile_ranges),
+                                  _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(rng),
+                                  _ptr(intensity), _ptr(raydrop), _ptr(alpha), C.c_void_p(stream)))

@@ -1,0 +1,119 @@
+"""Frame rendering through the C-ABI (buffer management + the four calls).
+
+`Renderer` keeps a surfel set resident on one GPU and renders sensor frames
+with gs_project -> gs_bin_sort -> gs_render_camera / gs_render_lidar.  It only
+allocates torch buffers and marshals arguments: every step of the path runs
+in libgsr.so.  Two sizing modes (include/gsr.h):
+
+  * exact (default): after gs_project it reads the pair count P (one device
+    sync) and sizes the pair buffers to P;
+  * capacity: a fixed pair capacity, no host sync (CUDA-graph capturable);
+    if the overflow flag is raised the frame is re-rendered with a larger
+    capacity (check with `overflowed()`).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import gsr
+
+CAMERA_CHANNELS = ("r", "g", "b", "depth", "nx", "ny", "nz", "alpha")
+LIDAR_CHANNELS = ("range", "intensity", "raydrop", "alpha")
+
+
+def to_device(s, device="cuda") -> dict:
+    """scenegen.Surfels (numpy fp32) -> dict of contiguous CUDA tensors."""
+    f = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
+    return dict(means=f(s.means), quats=f(s.quats), scales=f(s.scales), opacities=f(s.opacities),
+                sh=f(s.sh), sh_degree=int(s.sh_degree), intensity=f(s.intensity),
+                raydrop_logit=f(s.raydrop_logit))
+
+
+def n_channels(kind):
+    return 4 if kind == gsr.GS_LIDAR_SPINNING else 8
+
+
+class Renderer:
+    def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda"):
+        self.device = torch.device(device)
+        self.t = surfels
+        self.n = int(surfels["means"].shape[0])
+        self.struct = gsr.surfels_struct(surfels)
+        self.opts = opts if opts is not None else gsr.default_opts()
+        self._buf = {}
+        self.last_pairs = None
+
+    # buffers are cached per (name) and grown on demand
+    def _get(self, name, nbytes):
+        b = self._buf.get(name)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+            self._buf[name] = b
+        return b
+
+    def _i32(self, name, count):
+        return self._get(name, 4 * max(count, 1))[: 4 * max(count, 1)].view(torch.int32)
+
+    def project(self, sensor: gsr.Sensor, stream=None):
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        proj = self._get("proj", gsr.gs_projected_bytes(self.n, sensor.kind))
+        d_np = self._get("np", 8)[:8].view(torch.int64)
+        gsr.gs_project(self.struct, sensor, self.opts, proj, d_np, st)
+        return proj, d_np
+
+    def render(self, sensor, out: torch.Tensor | None = None, capacity: int | None = None,
+               keys: bool = False, stream=None) -> torch.Tensor:
+        """Render one frame; returns a planar fp32 tensor [C,H,W] (C = 8 for
+        cameras: r,g,b,depth,nx,ny,nz,alpha; 4 for LiDAR: range, intensity,
+        raydrop, alpha)."""
+        if not isinstance(sensor, gsr.Sensor):
+            sensor = gsr.Sensor(sensor)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        proj, d_np = self.project(sensor, st)
+        if capacity is None:
+            cap = int(d_np.item())   # exact sizing (one sync)
+        else:
+            cap = int(capacity)
+        self.last_pairs = cap
+        nt = gsr.gs_num_tiles(sensor, self.opts)
+        values = self._i32("values", cap)
+        ranges = self._i32("ranges", 2 * nt)
+        ovf = self._i32("overflow", 1)
+        ws = self._get("ws", gsr.gs_sort_workspace_bytes(self.n, cap, sensor, self.opts))
+        kbuf = self._get("keys", 8 * max(cap, 1))[: 8 * max(cap, 1)].view(torch.int64) if keys else None
+        gsr.gs_bin_sort(proj, self.n, sensor, self.opts, kbuf, values, cap, ranges, ws, ovf, st)
+        C = n_channels(sensor.kind)
+        H, W = sensor.height, sensor.width
+        if out is None:
+            out = torch.empty((C, H, W), dtype=torch.float32, device=self.device)
+        if sensor.kind == gsr.GS_LIDAR_SPINNING:
+            gsr.gs_render_lidar(proj, self.n, values, ranges, ovf, sensor, self.opts, out[0], out[1],
+                                out[2], out[3], st)
+        else:
+            gsr.gs_render_camera(proj, self.n, values, ranges, ovf, sensor, self.opts, out[0:3],
+                                 out[3], out[4:7], out[7], st)
+        self._last = dict(proj=proj, values=values, ranges=ranges, overflow=ovf, keys=kbuf, cap=cap,
+                          ntiles=nt, sensor=sensor)
+        return out
+
+    def overflowed(self) -> bool:
+        return bool(self._last["overflow"].item())
+
+    def binning_state(self):
+        """Host copies of the last frame's per-surfel and sorted-pair arrays
+        (for the bit-exact binning test)."""
+        L = self._last
+        sensor = L["sensor"]
+        offs = gsr.gs_projected_offsets(self.n, sensor.kind)
+        proj = L["proj"]
+        n = self.n
+        rect = proj[offs["rect"]: offs["rect"] + 8 * n].view(torch.int16).view(n, 4).cpu().numpy()
+        key = proj[offs["key"]: offs["key"] + 4 * n].view(torch.int32).cpu().numpy().view(np.uint32)
+        cnt = proj[offs["count"]: offs["count"] + 4 * n].view(torch.int32).cpu().numpy()
+        P = int(proj[8:16].view(torch.int64).item())
+        vals = L["values"][:P].cpu().numpy().view(np.uint32)
+        keys = L["keys"][:P].cpu().numpy().view(np.uint64) if L["keys"] is not None else None
+        ranges = L["ranges"][: 2 * L["ntiles"]].cpu().numpy().view(np.uint32).reshape(-1, 2)
+        return dict(rect=rect, key=key, count=cnt, P=P, values=vals, keys=keys, ranges=ranges,
+                    ntiles=L["ntiles"])

@@ -1,0 +1,93 @@
+"""Tolerance protocol of DESIGN.md §5 (GPU vs oracle), shared by GPU tests,
+smoke() and bench.py's parity spot check."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+TOL_ABS = 1e-4        # colour, alpha, normal, intensity, raydrop (north_star)
+TOL_REL = 1e-4        # depth, range (north_star)
+TOL_FLAGGED = 0.02    # near-decision rays: gross-error bound
+MAX_FLAGGED_FRAC = 2e-3
+
+
+def sample_rays(sensor, n_random=4096, n_tiles=16, tile=16, seed=0):
+    """All pixels of `n_tiles` random tiles plus `n_random` random pixels."""
+    rng = np.random.default_rng(seed)
+    W, H = sensor.width, sensor.height
+    ntx, nty = (W + tile - 1) // tile, (H + tile - 1) // tile
+    rays = []
+    for t in rng.choice(ntx * nty, min(n_tiles, ntx * nty), replace=False):
+        ty, tx = divmod(int(t), ntx)
+        ys, xs = np.meshgrid(np.arange(ty * tile, min(H, ty * tile + tile)),
+                             np.arange(tx * tile, min(W, tx * tile + tile)), indexing="ij")
+        rays.append((ys * W + xs).ravel())
+    rays.append(rng.choice(W * H, min(n_random, W * H), replace=False))
+    return np.unique(np.concatenate(rays)).astype(np.int64)
+
+
+def compare(gpu_chw: np.ndarray, ref: np.ndarray, flags: np.ndarray, rays: np.ndarray, sensor):
+    """gpu_chw: [C,H,W] GPU output; ref: [n,8] oracle output for `rays`.
+    Returns a stats dict; stats['ok'] tells whether the gate passed."""
+    W = sensor.width
+    cam = sensor.kind != oracle.LIDAR
+    C = 8 if cam else 4
+    g = gpu_chw.reshape(C, -1)[:, rays].T.astype(np.float64)
+    r = ref[:, :C]
+    fl = flags != 0
+    if cam:
+        abs_ch, rel_ch, a_ch = [0, 1, 2, 4, 5, 6, 7], 3, 7
+    else:
+        abs_ch, rel_ch, a_ch = [1, 2, 3], 0, 3
+    err_abs = np.abs(g[:, abs_ch] - r[:, abs_ch]).max(axis=1)
+    has = r[:, a_ch] > 0
+    rel = np.zeros(len(rays))
+    rel[has] = np.abs(g[has, rel_ch] - r[has, rel_ch]) / np.maximum(np.abs(r[has, rel_ch]), 1e-30)
+    empty_bad = (~has) & ((g[:, a_ch] != 0) | (g[:, rel_ch] != (0.0 if cam else r[:, rel_ch])))
+    bad = (~fl) & ((err_abs > TOL_ABS) | (rel > TOL_REL) | empty_bad)
+    bad_flagged = fl & (err_abs > TOL_FLAGGED)
+    stats = dict(n=len(rays), flagged=int(fl.sum()), bad=int(bad.sum()),
+                 bad_flagged=int(bad_flagged.sum()),
+                 max_abs_unflagged=float(err_abs[~fl].max()) if (~fl).any() else 0.0,
+                 p9999_abs=float(np.quantile(err_abs[~fl], 0.9999)) if (~fl).any() else 0.0,
+                 mean_abs=float(err_abs[~fl].mean()) if (~fl).any() else 0.0,
+                 max_rel_depth_unflagged=float(rel[~fl].max()) if (~fl).any() else 0.0,
+                 max_abs_flagged=float(err_abs[fl].max()) if fl.any() else 0.0)
+    stats["ok"] = (stats["bad"] == 0 and stats["bad_flagged"] == 0 and
+                   stats["flagged"] <= max(2, MAX_FLAGGED_FRAC * len(rays)))
+    if stats["bad"]:
+        i = np.nonzero(bad)[0][:5]
+        stats["worst"] = [dict(ray=int(rays[k]), x=int(rays[k] % W), y=int(rays[k] // W),
+                               gpu=g[k].round(7).tolist(), ref=r[k].round(7).tolist()) for k in i]
+    return stats
+
+
+def cpu_bin_sort(rect, key, ntx, ntiles):
+    """Reference binning from the GPU's own per-surfel arrays: enumerate each
+    visible surfel's tiles row-major (tile column modulo ntx), stable-sort the
+    pairs by (tile, depth-key bits, surfel index), extract [start,end) ranges."""
+    vis = np.nonzero((rect[:, 2] >= rect[:, 0]) & (rect[:, 3] >= rect[:, 1]))[0]
+    tiles, ids = [], []
+    for i in vis:
+        x0, y0, x1, y1 = (int(v) for v in rect[i])
+        ty, tx = np.meshgrid(np.arange(y0, y1 + 1), np.arange(x0, x1 + 1), indexing="ij")
+        t = ty * ntx + np.where(tx >= ntx, tx - ntx, tx)
+        tiles.append(t.ravel())
+        ids.append(np.full(t.size, i))
+    if not tiles:
+        return np.zeros(0, np.uint32), np.zeros(0, np.uint64), np.zeros((ntiles, 2), np.uint32)
+    tiles = np.concatenate(tiles).astype(np.uint64)
+    ids = np.concatenate(ids).astype(np.uint64)
+    kk = (tiles << np.uint64(32)) | key[ids.astype(np.int64)].astype(np.uint64)
+    order = np.lexsort((ids, kk))
+    vals = ids[order].astype(np.uint32)
+    keys = kk[order]
+    t_sorted = (keys >> np.uint64(32)).astype(np.int64)
+    ranges = np.zeros((ntiles, 2), np.uint32)
+    starts = np.searchsorted(t_sorted, np.arange(ntiles), side="left")
+    ends = np.searchsorted(t_sorted, np.arange(ntiles), side="right")
+    nz = ends > starts
+    ranges[nz, 0] = starts[nz]
+    ranges[nz, 1] = ends[nz]
+    return vals, keys, ranges

@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle
+(-m gpu).  Tolerance protocol: tests/parity.py / DESIGN.md §5."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import scenegen as sg  # noqa: E402
+from tests import parity  # noqa: E402
+from tests.helpers import empty_scene, scene  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def gsr_mod():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_11731_b200 import gsr
+    gsr.load()
+    return gsr
+
+
+def _render(surfels, sensor, **kw):
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.render import Renderer, to_device
+    opts = gsr.default_opts(**kw.pop("opts", {}))
+    r = Renderer(to_device(surfels), opts)
+    out = r.render(sensor, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), r
+
+
+def _check(surfels, sensor, rays=None, label=""):
+    img, _ = _render(surfels, sensor)
+    if rays is None:
+        rays = np.arange(sensor.width * sensor.height)
+    ref, fl, _ = oracle.render(surfels, sensor, rays)
+    st = parity.compare(img, ref, fl, rays, sensor)
+    print(label, {k: v for k, v in st.items() if k != "worst"})
+    assert st["ok"], st
+    return st
+
+
+# ---------------------------------------------------------------- full frames
+def test_tiny_full_frame(gsr_mod):
+    c = sg.tiny()
+    _check(c.surfels, c.sensors[0], label="tiny")
+
+
+def test_street_small_full_frame_ragged(gsr_mod):
+    """20K street surfels, 200x150 pinhole: several tiles plus ragged edges."""
+    c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+    _check(c.surfels, c.sensors[0], label="street-small")
+
+
+def test_fisheye_small_full_frame(gsr_mod):
+    rng = np.random.default_rng(12)
+    s = sg.street(rng, 30_000, 0.0, 60.0, 3)
+    k, _ = sg.draw_fisheye_k(rng, float(np.float32(np.deg2rad(95))))
+    se = sg.fisheye(176, 136, np.deg2rad(95), k, 88.0, 68.0, sg.camera_pose([0, 1.5, 0], 0.0))
+    _check(s, se, label="fisheye-small")
+
+
+def test_lidar_small_full_frame(gsr_mod):
+    rng = np.random.default_rng(13)
+    s = sg.street(rng, 60_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
+    se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
+    _check(s, se, label="lidar-small")
+
+
+# ---------------------------------------------------------------- BASELINE configs, sampled
+def test_mid_sampled(gsr_mod):
+    c = sg.mid()
+    se = c.sensors[0]
+    _check(c.surfels, se, parity.sample_rays(se, 2048, 8), label="mid")
+
+
+def test_fisheye_sampled(gsr_mod):
+    c = sg.fisheye_cfg()
+    se = c.sensors[0]
+    _check(c.surfels, se, parity.sample_rays(se, 1024, 4), label="fisheye")
+
+
+def test_lidar_sampled(gsr_mod):
+    c = sg.lidar_cfg()
+    se = c.sensors[0]
+    _check(c.surfels, se, parity.sample_rays(se, 1024, 4), label="lidar")
+
+
+# ---------------------------------------------------------------- binning, invariants
+def test_binning_bit_exact(gsr_mod):
+    """Keys, values and tile ranges equal a CPU stable sort of the GPU's own
+    per-surfel (rect, key) arrays; GPU keys equal the oracle's pinned keys."""
+    for c in [sg.tiny(), sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)]:
+        se = c.sensors[0]
+        img, r = _render(c.surfels, se, keys=True)
+        b = r.binning_state()
+        ntx = (se.width + 15) // 16
+        vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
+        assert b["P"] == len(vals)
+        np.testing.assert_array_equal(b["values"], vals)
+        np.testing.assert_array_equal(b["keys"], keys)
+        np.testing.assert_array_equal(b["ranges"], ranges)
+        okb, cul = oracle.keys(c.surfels, se)
+        vis = b["count"] > 0
+        np.testing.assert_array_equal(b["key"][vis], okb[vis])
+        assert not np.any(cul[vis])
+
+
+def test_binning_bit_exact_lidar_wrap(gsr_mod):
+    rng = np.random.default_rng(21)
+    s = sg.street(rng, 20_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
+    se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
+    img, r = _render(s, se, keys=True)
+    b = r.binning_state()
+    ntx = (se.width + 15) // 16
+    assert np.any(b["rect"][:, 2] >= ntx)   # some surfels straddle the azimuth seam
+    vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
+    np.testing.assert_array_equal(b["values"], vals)
+    np.testing.assert_array_equal(b["keys"], keys)
+    np.testing.assert_array_equal(b["ranges"], ranges)
+
+
+@pytest.mark.parametrize("tiles", [(8, 8), (32, 8), (16, 4)])
+def test_tile_shape_invariance_bitwise(gsr_mod, tiles):
+    c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+    a, _ = _render(c.surfels, c.sensors[0])
+    b, _ = _render(c.surfels, c.sensors[0], opts=dict(tile_w=tiles[0], tile_h=tiles[1]))
+    np.testing.assert_array_equal(a, b)
+
+
+def test_deterministic_repeat(gsr_mod):
+    c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+    a, _ = _render(c.surfels, c.sensors[0])
+    b, _ = _render(c.surfels, c.sensors[0])
+    np.testing.assert_array_equal(a, b)
+
+
+def test_empty_scene(gsr_mod):
+    se = sg.pinhole(40, 30, 30.0, 20.0, 15.0, sg.identity_pose())
+    img, _ = _render(empty_scene(), se)
+    assert np.all(img == 0)
+    li = sg.lidar64(sg.lidar_pose([0, 0, 0]), height=8, width=64)
+    img, _ = _render(empty_scene(), li)
+    assert np.all(img[[0, 1, 3]] == 0) and np.all(img[2] == 1.0)
+
+
+def test_single_surfel_closed_form(gsr_mod):
+    se = sg.pinhole(32, 24, 16.0, 16.0, 12.0, sg.identity_pose())
+    s = scene([dict(mu=[1.125, -0.375, 4.0], R=np.eye(3), s=(0.5, 0.5), o=0.7, rgb=(0.2, 0.6, 0.9))])
+    img, _ = _render(s, se)
+    a = np.float32(0.7)
+    assert abs(img[7, 10, 20] - a) < 1e-6
+    assert abs(img[3, 10, 20] - 4.0) < 4e-6
+    np.testing.assert_allclose(img[:3, 10, 20], a * np.array([0.2, 0.6, 0.9]), atol=1e-6)
+
+
+def test_capacity_overflow_and_graph_mode(gsr_mod):
+    c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.render import Renderer, to_device
+    r = Renderer(to_device(c.surfels))
+    exact = r.render(c.sensors[0]).cpu().numpy()
+    P = r.last_pairs
+    small = r.render(c.sensors[0], capacity=P // 2).cpu().numpy()
+    assert r.overflowed()
+    assert np.all(small[7] == 0)
+    big = r.render(c.sensors[0], capacity=P + 1000).cpu().numpy()
+    assert not r.overflowed()
+    np.testing.assert_array_equal(big, exact)
