@@ -17,7 +17,7 @@
  *     launch: GS_ERR_CONFIG (null required pointer, wrong sensor kind for the
  *     call, sh_degree outside 0..3, width/height < 1, buffer too small),
  *     GS_ERR_RANGE (focal <= 0, non-monotone beam table, azimuth span outside
- *     (0, 2pi], theta_max outside (0, pi), tile shape outside 1..1024
+ *     (0, 2pi], theta_max outside (0, pi), tile shape outside 1..512
  *     threads), GS_ERR_CUDA (launch failure, from cudaGetLastError).  On any
  *     error nothing is enqueued after the failing launch; gs_last_error()
  *     returns a thread-local message.  Non-finite surfel inputs are not an
@@ -93,7 +93,11 @@ typedef struct {
 
 /* Compositing constants (north_star); gs_default_opts() fills the defaults. */
 typedef struct {
-    int32_t tile_w, tile_h;      /* 16, 16 (camera) -- tile_w*tile_h threads per CTA     */
+    int32_t tile_w, tile_h;      /* 8 x 4: one tile = the samples of one warp;
+                                    tile_w*tile_h in 1..32 (LiDAR: 32 x 1 recommended) */
+    int32_t split_len;           /* tile lists longer than this are split into segments
+                                    composited in parallel and merged (0 = 2048;
+                                    INT32_MAX disables splitting)                        */
     float near_plane;            /* 0.2 m                                               */
     float alpha_max;             /* 0.99                                                */
     float alpha_min;             /* 1/255                                               */
@@ -161,22 +165,38 @@ gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sensor *sensor,
  *   rgb [3,H,W], depth [H,W] (normalised expected depth, 0 where alpha = 0),
  *   normal [3,H,W] (sensor frame, unnormalised composite), alpha [H,W].
  * d_overflow (may be NULL) is gs_bin_sort's flag: if set, outputs are background.
+ * workspace: device scratch of >= gs_render_workspace_bytes(pair_capacity, ...)
+ * bytes (the pair_capacity given to gs_bin_sort): the longest-first tile
+ * schedule and the partial composites of split tile lists.
+ * stats (may be NULL): device [2,H,W] u32 diagnostic counts per sample --
+ * surfels composited, (sample, surfel) pairs whose conservative pixel box
+ * contains the sample.  Non-NULL selects an instrumented kernel.
+ * Tiles whose list is shorter than opts->split_len are composited exactly in
+ * list order (bitwise independent of the tile shape); longer lists are
+ * composited in segments and merged with the transmittance prefix
+ * C = sum_k (prod_{j<k} T_j) C_k, re-walking the segment where the ray
+ * stops (exact stop rule; agrees with the unsplit result to fp32 rounding).
  */
+size_t gs_render_workspace_bytes(int64_t pair_capacity, const gs_sensor *sensor,
+                                 const gs_opts *opts);
+
 gs_status gs_render_camera(const void *projected, int64_t n, const uint32_t *values,
                            const uint32_t *tile_ranges, const int32_t *d_overflow,
-                           const gs_sensor *sensor, const gs_opts *opts, float *rgb,
-                           float *depth, float *normal, float *alpha, gs_stream stream);
+                           const gs_sensor *sensor, const gs_opts *opts, void *workspace,
+                           size_t workspace_bytes, float *rgb, float *depth, float *normal,
+                           float *alpha, uint32_t *stats, gs_stream stream);
 
 /*
  * gs_render_lidar -- range-image compositing (Eq. 5; ray-drop and
  * intensity).  Outputs planar fp32 [H,W] each (any may be NULL
  * except alpha): range (0 = no return), intensity, raydrop probability
- * (composited with background 1), alpha.
+ * (composited with background 1), alpha.  stats as for gs_render_camera.
  */
 gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *values,
                           const uint32_t *tile_ranges, const int32_t *d_overflow,
-                          const gs_sensor *sensor, const gs_opts *opts, float *range,
-                          float *intensity, float *raydrop, float *alpha, gs_stream stream);
+                          const gs_sensor *sensor, const gs_opts *opts, void *workspace,
+                          size_t workspace_bytes, float *range, float *intensity,
+                          float *raydrop, float *alpha, uint32_t *stats, gs_stream stream);
 
 const char *gs_status_string(gs_status status);
 const char *gs_last_error(void);

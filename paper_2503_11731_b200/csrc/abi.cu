@@ -14,12 +14,13 @@ size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles);
 cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
                             int32_t *d_overflow, cudaStream_t st);
+size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len);
 cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
-                                 const int32_t *, const DevSensor &, const DevOpts &, float *, float *,
-                                 float *, float *, cudaStream_t);
+                                 const int32_t *, const DevSensor &, const DevOpts &, int32_t, void *,
+                                 size_t, float *, float *, float *, float *, uint32_t *, cudaStream_t);
 cudaError_t launch_render_lidar(const void *, int64_t, const uint32_t *, const uint32_t *,
-                                const int32_t *, const DevSensor &, const DevOpts &, float *, float *,
-                                float *, float *, cudaStream_t);
+                                const int32_t *, const DevSensor &, const DevOpts &, int32_t, void *,
+                                size_t, float *, float *, float *, float *, uint32_t *, cudaStream_t);
 }  // namespace gsr
 
 using namespace gsr;
@@ -37,8 +38,9 @@ static gs_status cuda_fail(cudaError_t e, const char *where) {
 
 extern "C" void gs_default_opts(gs_opts *o) {
     if (!o) return;
-    o->tile_w = 16;
-    o->tile_h = 16;
+    o->tile_w = 8;
+    o->tile_h = 4;
+    o->split_len = 0;
     o->near_plane = 0.2f;
     o->alpha_max = 0.99f;
     o->alpha_min = 1.0f / 255.0f;
@@ -65,8 +67,9 @@ extern "C" void gs_projected_offsets(int64_t n, int32_t kind, size_t offs[5]) {
 
 static gs_status check_opts(const gs_opts *o) {
     if (!o) return fail(GS_ERR_CONFIG, "opts is NULL");
-    if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 1024)
-        return fail(GS_ERR_RANGE, "tile shape must give 1..1024 threads per CTA");
+    if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 32)
+        return fail(GS_ERR_RANGE, "tile shape must hold 1..32 samples (one warp)");
+    if (o->split_len < 0) return fail(GS_ERR_RANGE, "split_len must be >= 0");
     if (!(o->near_plane > 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max <= 1.f) ||
         !(o->alpha_min >= 0.f) || !(o->t_min >= 0.f) || !(o->support_rho > 0.f) ||
         !(o->lowpass_sigma_px > 0.f))
@@ -212,36 +215,54 @@ extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sens
     return GS_OK;
 }
 
+extern "C" size_t gs_render_workspace_bytes(int64_t cap, const gs_sensor *s, const gs_opts *o) {
+    const int64_t nt = gs_num_tiles(s, o);
+    if (nt < 0 || cap < 0) return 0;
+    return render_workspace_bytes(cap, nt, o->split_len);
+}
+
+static gs_status check_render(const void *projected, const uint32_t *tile_ranges, const float *alpha,
+                              const gs_sensor *s, const gs_opts *o, void *ws, size_t ws_bytes) {
+    if (!projected || !tile_ranges || !alpha || !ws) return fail(GS_ERR_CONFIG, "null buffer");
+    if (ws_bytes < render_workspace_bytes(0, gs_num_tiles(s, o), o->split_len))
+        return fail(GS_ERR_CONFIG, "render workspace too small");
+    return GS_OK;
+}
+
 extern "C" gs_status gs_render_camera(const void *projected, int64_t n, const uint32_t *values,
                                       const uint32_t *tile_ranges, const int32_t *d_overflow,
-                                      const gs_sensor *s, const gs_opts *o, float *rgb, float *depth,
-                                      float *normal, float *alpha, gs_stream stream) {
+                                      const gs_sensor *s, const gs_opts *o, void *workspace,
+                                      size_t workspace_bytes, float *rgb, float *depth, float *normal,
+                                      float *alpha, uint32_t *stats, gs_stream stream) {
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
     if (s->kind == GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_camera called with a LiDAR sensor");
-    if (!projected || !tile_ranges || !alpha) return fail(GS_ERR_CONFIG, "null buffer");
+    if ((st = check_render(projected, tile_ranges, alpha, s, o, workspace, workspace_bytes)) != GS_OK) return st;
     const DevSensor se = make_dev_sensor(s, o);
     const DevOpts op = make_dev_opts(o);
-    cudaError_t e = launch_render_camera(projected, n, values, tile_ranges, d_overflow, se, op, rgb, depth, normal,
-                                         alpha, (cudaStream_t)stream);
+    cudaError_t e = launch_render_camera(projected, n, values, tile_ranges, d_overflow, se, op, o->split_len,
+                                         workspace, workspace_bytes, rgb, depth, normal, alpha, stats,
+                                         (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_render_camera");
     return GS_OK;
 }
 
 extern "C" gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *values,
                                      const uint32_t *tile_ranges, const int32_t *d_overflow,
-                                     const gs_sensor *s, const gs_opts *o, float *range, float *intensity,
-                                     float *raydrop, float *alpha, gs_stream stream) {
+                                     const gs_sensor *s, const gs_opts *o, void *workspace,
+                                     size_t workspace_bytes, float *range, float *intensity, float *raydrop,
+                                     float *alpha, uint32_t *stats, gs_stream stream) {
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
     if (s->kind != GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_lidar called with a camera sensor");
-    if (!projected || !tile_ranges || !alpha) return fail(GS_ERR_CONFIG, "null buffer");
+    if ((st = check_render(projected, tile_ranges, alpha, s, o, workspace, workspace_bytes)) != GS_OK) return st;
     const DevSensor se = make_dev_sensor(s, o);
     const DevOpts op = make_dev_opts(o);
-    cudaError_t e = launch_render_lidar(projected, n, values, tile_ranges, d_overflow, se, op, range, intensity,
-                                        raydrop, alpha, (cudaStream_t)stream);
+    cudaError_t e = launch_render_lidar(projected, n, values, tile_ranges, d_overflow, se, op, o->split_len,
+                                        workspace, workspace_bytes, range, intensity, raydrop, alpha, stats,
+                                        (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_render_lidar");
     return GS_OK;
 }

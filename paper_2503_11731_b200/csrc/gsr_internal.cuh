@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/gsr.h"
 
@@ -48,17 +49,31 @@ struct DevSurfels {
 enum : int {
     PH_A00 = 0, PH_A01, PH_A10, PH_A11, PH_A20, PH_A21, PH_QC, PH_RCUT3,
     PH_CHX = 8, PH_CHY, PH_CLX, PH_CLY, PH_RCUT2, PH_O, PH_DET, PH_ZC,
-    PH_R = 16, PH_G, PH_B, PH_NX, PH_NY, PH_NZ, PH_FLOATS = 24
+    PH_R = 16, PH_G, PH_B, PH_NX, PH_NY, PH_NZ, PH_BBX, PH_BBY, PH_FLOATS = 24
 };
+// PH_BBX / PH_BBY (and FE_, LI_ alike): conservative pixel bounding box of the
+// surfel's support, inclusive, as two packed u16 pairs (lo | hi << 16); for
+// LiDAR the column range may run past width-1 (azimuth wrap).
 // Fisheye / LiDAR (ray direction d = m + e, m = unit centre direction,
 // stored hi+lo): u = U.e / D, v = V.e / D, range t = rdet / D, D = det + N.e.
 enum : int {
     RY_MH = 0, RY_RCUT3 = 3, RY_ML = 4, RY_DET = 7, RY_U = 8, RY_O = 11, RY_V = 12, RY_RDET = 15,
     RY_N = 16, RY_RC = 19,
-    FE_CHX = 20, FE_CHY, FE_CLX, FE_CLY, FE_RCUT2, FE_PAD0, FE_PAD1, FE_PAD2,
+    FE_CHX = 20, FE_CHY, FE_CLX, FE_CLY, FE_RCUT2, FE_PAD0, FE_BBX, FE_BBY,
     FE_R = 28, FE_G, FE_B, FE_NX, FE_NY, FE_NZ, FE_FLOATS = 36,
-    LI_INT = 20, LI_DROP = 21, LI_FLOATS = 24
+    LI_INT = 20, LI_DROP = 21, LI_BBX = 22, LI_BBY = 23, LI_FLOATS = 24
 };
+
+__host__ __device__ inline float pack_bb(int lo, int hi) {
+    const uint32_t u = ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(u);
+#else
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+#endif
+}
 
 __host__ __device__ inline int record_floats(int kind) {
     return kind == GS_PINHOLE ? (int)PH_FLOATS : (kind == GS_FISHEYE_EQUIDISTANT ? (int)FE_FLOATS : (int)LI_FLOATS);

@@ -90,7 +90,7 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
 
 // pixel range [i0,i1] -> tile range; returns false if empty
 __device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw, int th,
-                                             int &tx0, int &ty0, int &tx1, int &ty1) {
+                                             int &tx0, int &ty0, int &tx1, int &ty1, int pb[4]) {
     const double m = 1e-3;
     double x0 = bx.x0 - m - 1e-6 * fabs(bx.x0), x1 = bx.x1 + m + 1e-6 * fabs(bx.x1);
     double y0 = bx.y0 - m - 1e-6 * fabs(bx.y0), y1 = bx.y1 + m + 1e-6 * fabs(bx.y1);
@@ -103,6 +103,7 @@ __device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw
     const int cj0 = (int)fmax(j0, 0.0), cj1 = (int)fmin(j1, (double)(H - 1));
     if (ci0 > ci1 || cj0 > cj1) return false;
     tx0 = ci0 / tw; tx1 = ci1 / tw; ty0 = cj0 / th; ty1 = cj1 / th;
+    pb[0] = ci0; pb[1] = cj0; pb[2] = ci1; pb[3] = cj1;
     return true;
 }
 
@@ -175,6 +176,95 @@ __device__ __forceinline__ bool beam_rows(const DevSensor &se, double lo, double
     return r0 <= r1;
 }
 
+// Angular box of a surfel's support as seen from the sensor origin:
+// elevation above the sensor's xy plane in [el_lo, el_hi]; azimuth about z in
+// azc + [daz_lo, daz_hi] unless all_az.
+struct AngBox {
+    double el_lo, el_hi, azc, daz_lo, daz_hi;
+    bool all_az;
+};
+
+// Range of the linear-fractional f(c,s) = (n0 + n1 c + n2 s)/(d0 + d1 c + d2 s)
+// over the unit disk (denominator > 0 on it): the extremes lie on the circle
+// at the two roots of A c + B s + C = 0.
+__device__ void lf_range(double n0, double n1, double n2, double d0, double d1, double d2, double &lo,
+                         double &hi) {
+    lo = hi = n0 / d0;
+    const double A = n2 * d0 - n0 * d2, B = n0 * d1 - n1 * d0, C = n2 * d1 - n1 * d2;
+    const double rr = A * A + B * B;
+    if (rr > 0.0) {
+        const double q = sqrt(fmax(rr - C * C, 0.0));
+        const double cs[2][2] = {{(-A * C + B * q) / rr, (-B * C - A * q) / rr},
+                                 {(-A * C - B * q) / rr, (-B * C + A * q) / rr}};
+        for (int k = 0; k < 2; ++k) {
+            const double f = (n0 + n1 * cs[k][0] + n2 * cs[k][1]) / (d0 + d1 * cs[k][0] + d2 * cs[k][1]);
+            lo = fmin(lo, f);
+            hi = fmax(hi, f);
+        }
+    }
+    for (int k = 0; k < 4; ++k) {   // safety points on the circle
+        const double c = k == 0 ? 1.0 : (k == 1 ? -1.0 : 0.0), s = k == 2 ? 1.0 : (k == 3 ? -1.0 : 0.0);
+        const double f = (n0 + n1 * c + n2 * s) / (d0 + d1 * c + d2 * s);
+        lo = fmin(lo, f);
+        hi = fmax(hi, f);
+    }
+}
+
+// Exact-extreme bound of the disk {mu + c a + s b : c^2+s^2 <= 1} through the
+// gnomonic projection at the centre direction m (lines of the projection are
+// great circles): xi = P.e_az / P.m, eta = P.e_el / P.m are linear-fractional
+// in (c,s); the direction m + xi e_az + eta e_el then bounds elevation and
+// azimuth with numerator/denominator interval arithmetic.  Returns false if
+// the disk reaches the plane P.m = 0 or the centre is at the pole.
+__device__ bool angular_box_disk(const double mu[3], const double a[3], const double b[3], AngBox &ab) {
+    const double r = sqrt(dot3(mu, mu));
+    const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
+    const double rho = sqrt(m[0] * m[0] + m[1] * m[1]);
+    if (!(rho > 1e-6)) return false;
+    const double eaz[3] = {-m[1] / rho, m[0] / rho, 0.0};
+    const double eel[3] = {-m[2] * m[0] / rho, -m[2] * m[1] / rho, rho};
+    const double d1 = dot3(a, m), d2 = dot3(b, m);
+    if (!(r - sqrt(d1 * d1 + d2 * d2) > 1e-3 * r)) return false;
+    double xl, xh, yl, yh;
+    lf_range(0.0, dot3(a, eaz), dot3(b, eaz), r, d1, d2, xl, xh);
+    lf_range(0.0, dot3(a, eel), dot3(b, eel), r, d1, d2, yl, yh);
+    const double mg = 1e-9;
+    xl -= mg; xh += mg; yl -= mg; yh += mg;
+    // elevation: sin(el) = (m_z + eta*rho) / sqrt(1 + xi^2 + eta^2)
+    const double x2lo = (xl <= 0.0 && xh >= 0.0) ? 0.0 : fmin(xl * xl, xh * xh), x2hi = fmax(xl * xl, xh * xh);
+    const double y2lo = (yl <= 0.0 && yh >= 0.0) ? 0.0 : fmin(yl * yl, yh * yh), y2hi = fmax(yl * yl, yh * yh);
+    const double den_lo = sqrt(1.0 + x2lo + y2lo), den_hi = sqrt(1.0 + x2hi + y2hi);
+    const double nlo = m[2] + yl * rho, nhi = m[2] + yh * rho;
+    const double shi = nhi > 0.0 ? nhi / den_lo : nhi / den_hi;
+    const double slo = nlo > 0.0 ? nlo / den_hi : nlo / den_lo;
+    ab.el_hi = asin(fmin(1.0, shi)) + 1e-7;
+    ab.el_lo = asin(fmax(-1.0, slo)) - 1e-7;
+    // azimuth: tan(daz) = xi / (rho - eta*m_z)
+    const double t1 = yl * m[2], t2 = yh * m[2];
+    const double Dlo = rho - fmax(t1, t2), Dhi = rho - fmin(t1, t2);
+    ab.azc = atan2(m[1], m[0]);
+    ab.all_az = !(Dlo > 1e-9) || ab.el_hi >= 0.5 * M_PI || ab.el_lo <= -0.5 * M_PI;
+    if (!ab.all_az) {
+        ab.daz_hi = atan(xh > 0.0 ? xh / Dlo : xh / Dhi) + 1e-7;
+        ab.daz_lo = atan(xl < 0.0 ? xl / Dlo : xl / Dhi) - 1e-7;
+    }
+    return true;
+}
+
+// Sphere-cap fallback: all directions within beta of the centre direction.
+__device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
+    const double elc = asin(fmin(1.0, fmax(-1.0, m[2])));
+    ab.el_lo = elc - beta;
+    ab.el_hi = elc + beta;
+    ab.azc = atan2(m[1], m[0]);
+    ab.all_az = beta >= 0.5 * M_PI - fabs(elc);
+    if (!ab.all_az) {
+        const double sb = sin(beta) / cos(elc);
+        if (sb >= 1.0) ab.all_az = true;
+        else { ab.daz_hi = asin(sb); ab.daz_lo = -ab.daz_hi; }
+    }
+}
+
 // ------------------------------------------------------------------ projection
 template <int KIND>
 __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_constant__ DevSensor se,
@@ -207,6 +297,7 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
     const float su = __ldg(s.scales + 2 * i), sv = __ldg(s.scales + 2 * i + 1);
     vis = vis && (su > 0.f) && (sv > 0.f) && isfinite(su) && isfinite(sv);
     int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+    int pb[4] = {0, 0, -1, -1};   // conservative pixel bbox (x0,y0,x1,y1), inclusive
     double A[3], Bv[3], N[3];
     if (vis) {
         const float4 qf = __ldg(reinterpret_cast<const float4 *>(s.quats) + i);
@@ -238,13 +329,20 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
             const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
             bx.add(cx - rlp, cy - rlp);
             bx.add(cx + rlp, cy + rlp);
-            vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1);
+            vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1, pb);
         } else {
             const double r = sqrt(dot3(mu, mu));
             const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
             const double R3 = Rr * (double)fmaxf(su, sv);
             const bool whole = !(R3 < 0.999 * r);
-            const double beta = whole ? 0.0 : asin(R3 / r);
+            // angular box of the support disk (elevation above the sensor xy
+            // plane, azimuth about z): exact gnomonic extremes, else sphere cap
+            AngBox ab;
+            if (!whole) {
+                double a[3], b[3];
+                for (int k = 0; k < 3; ++k) { a[k] = Rr * su * A[k]; b[k] = Rr * sv * Bv[k]; }
+                if (!angular_box_disk(mu, a, b, ab)) angular_box_cap(m, asin(R3 / r), ab);
+            }
             if (KIND == GS_FISHEYE_EQUIDISTANT) {
                 Box bx;
                 bx.init();
@@ -254,22 +352,16 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
                     bx.add(se.cx - se.fx * rad, se.cy - se.fy * rad);
                     bx.add(se.cx + se.fx * rad, se.cy + se.fy * rad);
                 } else {
-                    const double thc = acos(fmin(1.0, fmax(-1.0, m[2])));
-                    const double thlo = fmax(0.0, thc - beta), thhi = fmin(tm, thc + beta);
+                    // polar angle from the optical axis theta = pi/2 - elevation
+                    const double thlo = fmax(0.0, 0.5 * M_PI - ab.el_hi), thhi = fmin(tm, 0.5 * M_PI - ab.el_lo);
                     if (thlo <= tm) {
                         const double r0 = kb_theta_d(se, thlo), r1 = kb_theta_d(se, thhi);
-                        bool allpsi = (beta >= thc) || (thc + beta >= M_PI);
-                        double dpsi = M_PI;
-                        if (!allpsi) {
-                            const double sb = sin(beta) / sin(thc);
-                            if (sb >= 1.0) allpsi = true; else dpsi = asin(sb);
-                        }
+                        const bool allpsi = ab.all_az || thlo <= 0.0;
                         if (allpsi) {
                             bx.add(se.cx - se.fx * r1, se.cy - se.fy * r1);
                             bx.add(se.cx + se.fx * r1, se.cy + se.fy * r1);
                         } else {
-                            const double psic = atan2(m[1], m[0]);
-                            const double p0 = psic - dpsi, p1 = psic + dpsi;
+                            const double p0 = ab.azc + ab.daz_lo, p1 = ab.azc + ab.daz_hi;
                             const double rads[2] = {r0, r1};
                             for (int k = 0; k < 2; ++k) {
                                 bx.add(se.cx + se.fx * rads[k] * cos(p0), se.cy + se.fy * rads[k] * sin(p0));
@@ -290,26 +382,19 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
                 fisheye_project(se, mu, cxp, cyp);
                 bx.add(cxp - rlp, cyp - rlp);
                 bx.add(cxp + rlp, cyp + rlp);
-                vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1);
+                vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1, pb);
             } else {   // LiDAR: angular box with azimuth wrap
                 const int W = se.width;
                 int r0 = 0, r1 = se.nbeams - 1, c0 = 0, c1 = W - 1;
                 bool allaz = whole;
                 if (!whole) {
-                    const double elc = asin(fmin(1.0, fmax(-1.0, m[2])));
                     const double eps = 1e-6;
-                    vis = beam_rows(se, elc - beta - eps, elc + beta + eps, r0, r1);
-                    if (beta >= 0.5 * M_PI - fabs(elc)) allaz = true;
-                    double daz = M_PI;
+                    vis = beam_rows(se, ab.el_lo - eps, ab.el_hi + eps, r0, r1);
+                    allaz = ab.all_az;
                     if (!allaz) {
-                        const double sb = sin(beta) / cos(elc);
-                        if (sb >= 1.0) allaz = true; else daz = asin(sb);
-                    }
-                    if (!allaz) {
-                        const double azc = atan2(m[1], m[0]);
                         const double step = (double)se.az_step;
-                        const double ulo = (azc - daz - (double)se.az0) / step;
-                        const double uhi = (azc + daz - (double)se.az0) / step;
+                        const double ulo = (ab.azc + ab.daz_lo - (double)se.az0) / step;
+                        const double uhi = (ab.azc + ab.daz_hi - (double)se.az0) / step;
                         double jlo = ceil(ulo) - 1.0, jhi = floor(uhi) + 1.0;
                         if (se.full_turn) {
                             if (jhi - jlo + 1.0 >= (double)W) {
@@ -338,13 +423,15 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
                     const int ntx = se.ntx;
                     if (allaz) {
                         tx0 = 0; tx1 = ntx - 1;
+                        c0 = 0; c1 = W - 1;
                     } else {
                         tx0 = c0 / se.tw;
                         tx1 = c1 < W ? c1 / se.tw : ntx + (c1 - W) / se.tw;
-                        if (tx1 - tx0 + 1 >= ntx) { tx0 = 0; tx1 = ntx - 1; }
+                        if (tx1 - tx0 + 1 >= ntx) { tx0 = 0; tx1 = ntx - 1; c0 = 0; c1 = W - 1; }
                     }
                     ty0 = r0 / se.th;
                     ty1 = r1 / se.th;
+                    pb[0] = c0; pb[1] = r0; pb[2] = c1; pb[3] = r1;   // c1 may exceed W-1 (wrap)
                 }
             }
         }
@@ -395,7 +482,8 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
         sh_colour(s.sh + (size_t)i * nc * 3, s.sh_degree, vx * vn, vy * vn, vz * vn, rgb);
         R[PH_R] = rgb[0]; R[PH_G] = rgb[1]; R[PH_B] = rgb[2];
         R[PH_NX] = nsx; R[PH_NY] = nsy; R[PH_NZ] = nsz;
-        R[22] = 0.f; R[23] = 0.f;
+        R[PH_BBX] = pack_bb(pb[0], pb[2]);
+        R[PH_BBY] = pack_bb(pb[1], pb[3]);
         float4 *dst = reinterpret_cast<float4 *>(rec + (size_t)i * PH_FLOATS);
 #pragma unroll
         for (int k = 0; k < PH_FLOATS / 4; ++k)
@@ -435,10 +523,14 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
             sh_colour(s.sh + (size_t)i * nc * 3, s.sh_degree, vx * vn, vy * vn, vz * vn, rgb);
             R[FE_R] = rgb[0]; R[FE_G] = rgb[1]; R[FE_B] = rgb[2];
             R[FE_NX] = nsx; R[FE_NY] = nsy; R[FE_NZ] = nsz;
+            R[FE_BBX] = pack_bb(pb[0], pb[2]);
+            R[FE_BBY] = pack_bb(pb[1], pb[3]);
         } else {
             R[LI_INT] = s.inten ? __ldg(s.inten + i) : 0.f;
             const float lg = s.drop ? __ldg(s.drop + i) : 0.f;
             R[LI_DROP] = (float)(1.0 / (1.0 + exp(-(double)lg)));
+            R[LI_BBX] = pack_bb(pb[0], pb[2]);
+            R[LI_BBY] = pack_bb(pb[1], pb[3]);
         }
         float4 *dst = reinterpret_cast<float4 *>(rec + (size_t)i * NF);
 #pragma unroll

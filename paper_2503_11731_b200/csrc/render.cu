@@ -1,18 +1,26 @@
-// render.cu -- front-to-back compositing kernels (gs_render_camera,
-// gs_render_lidar).  PAPER.md Eq. 2 ray-splat intersection with the
-// unified plane pair (Eq. 3 pinhole, Eq. 5 LiDAR, equidistant fisheye per
-// DESIGN R4); 2DGS low-pass floor for cameras; north_star rule
-// alpha = min(alpha_max, o G), skip alpha < alpha_min, stop before
-// T < t_min.
+// render.cu -- front-to-back compositing (gs_render_camera, gs_render_lidar).
 //
-// One CTA per tile, one thread per pixel / LiDAR ray.  Surfel records of the
-// tile's depth-sorted list are staged in shared memory in batches of
-// blockDim records with cp.async (double buffered); every thread walks the
-// batch in order.  The plane pair of a sample meets the surfel where
-// (M^T h_u) x (M^T h_v) = det(M) M^{-1} (h_u x h_v), so the kernels evaluate
-// the adjugate of the surfel map on the ray direction; records are written
-// relative to the surfel centre so the fp32 arithmetic here
-// stays well conditioned.  No atomics: outputs are bitwise deterministic.
+// PAPER.md Eq. 2 ray-splat intersection with the unified plane pair
+// (Eq. 3 pinhole, Eq. 5 LiDAR, equidistant fisheye per DESIGN R4); 2DGS
+// low-pass floor for cameras; north_star rule alpha = min(alpha_max,
+// o G), skip alpha < alpha_min, stop before T < t_min.
+//
+// Work decomposition (B200): a tile is the 32 samples of ONE warp (8x4
+// pixels, or 32 LiDAR columns of one beam).  Warps are persistent: they pull
+// work items from a longest-first schedule built on the device, stage their
+// tile's depth-sorted surfel records into warp-private shared memory with
+// cp.async (32 records per batch, double buffered) and walk them in order.
+// Lists longer than split_len are cut into segments that run in parallel; a
+// merge kernel combines the segment composites with the transmittance prefix
+// and re-walks the one segment in which a ray stops, so the stop rule stays
+// exact.  No atomics touch the outputs: results are bitwise deterministic.
+//
+// The plane pair of a sample meets the surfel where
+// (M^T h_u) x (M^T h_v) = det(M) M^{-1} (h_u x h_v): the kernels evaluate the
+// adjugate of the surfel map on the ray direction.  Records are written
+// relative to the surfel centre so that fp32 suffices here.
+#include <algorithm>
+
 #include "gsr_internal.cuh"
 
 namespace gsr {
@@ -36,47 +44,80 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr float LOG2E_HALF = 0.72134752044448170368f;   // 0.5 * log2(e)
+constexpr int WARPS = 8;                                 // warps per CTA
+constexpr int NB = 32;                                   // schedule buckets
+constexpr int NPART = 10;                                // floats per partial composite
+constexpr uint32_t DEFAULT_SPLIT = 2048;
 
-template <int R4>
-__device__ __forceinline__ void stage_batch(float4 *dst, const float4 *__restrict__ rec,
-                                            const uint32_t *__restrict__ values, uint32_t first,
-                                            uint32_t cnt) {
-    const uint32_t t = threadIdx.x;
-    if (t < cnt) {
-        const uint32_t id = __ldg(values + first + t);
-        const float4 *src = rec + (size_t)id * R4;
-        float4 *d = dst + t * R4;
-#pragma unroll
-        for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
+template <int KIND> struct Rec;
+template <> struct Rec<GS_PINHOLE> { static constexpr int F = PH_FLOATS, BB = PH_BBX; };
+template <> struct Rec<GS_FISHEYE_EQUIDISTANT> { static constexpr int F = FE_FLOATS, BB = FE_BBX; };
+template <> struct Rec<GS_LIDAR_SPINNING> { static constexpr int F = LI_FLOATS, BB = LI_BBX; };
+
+// ---------------------------------------------------------------- workspace
+struct SchedHdr {
+    uint32_t counter;        // persistent work counter
+    uint32_t n_items;
+    uint32_t n_split;        // tiles whose list was split
+    uint32_t slot_cursor;    // partial-slot allocator
+    uint32_t seg_len;        // segment length L in use
+    uint32_t pad0[3];
+    uint32_t bucket_cnt[NB];
+    uint32_t bucket_cur[NB];
+    uint32_t pad1[24];
+};
+static_assert(sizeof(SchedHdr) == 384, "hdr");
+
+struct RenderWs {
+    size_t hdr, items, split_base, split_list, partials, total;
+    uint32_t max_items, max_split, max_slots, L;
+    RenderWs(int64_t cap, int64_t ntiles, int32_t split_len) {
+        L = split_len > 0 ? (uint32_t)split_len : DEFAULT_SPLIT;
+        const uint64_t c = (uint64_t)(cap > 0 ? cap : 0);
+        max_items = (uint32_t)(ntiles + c / L + 1);
+        max_split = (uint32_t)std::min<uint64_t>((uint64_t)ntiles, c / L + 1);
+        max_slots = (uint32_t)(2 * (c / L) + 2);
+        size_t o = 0;
+        hdr = o; o += 512;
+        items = o; o += align256((size_t)max_items * 8);
+        split_base = o; o += align256((size_t)ntiles * 4);
+        split_list = o; o += align256((size_t)max_split * 4);
+        partials = o; o += align256((size_t)max_slots * 32 * NPART * 4);
+        total = o;
     }
-    cp_async_commit();
-}
+};
 
-// ------------------------------------------------------------------ camera
+// ---------------------------------------------------------------- per-sample state
+struct Ray {
+    float px, py;            // pixel centre (cameras)
+    int pxi, pyi, pxw;       // integer sample coordinates, wrapped column (LiDAR seam)
+    float dh[3], dl[3];      // unit ray direction, hi + lo (fisheye, LiDAR)
+    bool inside, valid;
+};
+
+struct Acc {
+    float T, A, c0, c1, c2, d, n0, n1, n2;
+};
+
 template <int KIND>
-__global__ void __launch_bounds__(1024) k_render_camera(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
-    const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
-    const __grid_constant__ DevSensor se, const DevOpts op, float *__restrict__ out_rgb,
-    float *__restrict__ out_depth, float *__restrict__ out_normal, float *__restrict__ out_alpha) {
-    constexpr int R4 = (KIND == GS_PINHOLE ? PH_FLOATS : FE_FLOATS) / 4;
-    extern __shared__ float4 smem[];
-    const int B = blockDim.x;
-    const int tile = blockIdx.x;
+__device__ __forceinline__ Ray make_ray(const DevSensor &se, int tile, int lane) {
+    Ray ry;
     const int tyi = tile / se.ntx, txi = tile - tyi * se.ntx;
-    const int lx = threadIdx.x % se.tw, ly = threadIdx.x / se.tw;
-    const int pxi = txi * se.tw + lx, pyi = tyi * se.th + ly;
-    const bool inside = (lx < se.tw) && (ly < se.th) && pxi < se.width && pyi < se.height;
-    const float px = (float)pxi + 0.5f, py = (float)pyi + 0.5f;
-
-    bool valid = inside;
-    float dhx = 0.f, dhy = 0.f, dhz = 0.f, dlx = 0.f, dly = 0.f, dlz = 0.f;
-    if (KIND == GS_FISHEYE_EQUIDISTANT && inside) {
-        // ray of the pixel in fp64: invert theta_d = theta (1 + k1 t^2 + ...)
-        const double mx = __ddiv_rn(__dadd_rn((double)px, -(double)se.cx), (double)se.fx);
-        const double my = __ddiv_rn(__dadd_rn((double)py, -(double)se.cy), (double)se.fy);
+    const int lx = lane % se.tw, ly = lane / se.tw;
+    ry.pxi = txi * se.tw + lx;
+    ry.pyi = tyi * se.th + ly;
+    ry.pxw = ry.pxi + se.width;
+    ry.inside = lane < se.tw * se.th && ry.pxi < se.width && ry.pyi < se.height;
+    ry.px = (float)ry.pxi + 0.5f;
+    ry.py = (float)ry.pyi + 0.5f;
+    ry.valid = ry.inside;
+    for (int k = 0; k < 3; ++k) ry.dh[k] = ry.dl[k] = 0.f;
+    if (KIND == GS_FISHEYE_EQUIDISTANT && ry.inside) {
+        // invert theta_d = theta (1 + k1 t^2 + k2 t^4 + k3 t^6 + k4 t^8) (Newton, fp64)
+        const double mx = __ddiv_rn(__dadd_rn((double)ry.px, -(double)se.cx), (double)se.fx);
+        const double my = __ddiv_rn(__dadd_rn((double)ry.py, -(double)se.cy), (double)se.fy);
         const double td = __dsqrt_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)));
-        valid = td <= se.tdmax;
+        ry.valid = td <= se.tdmax;
         const double tdc = fmin(td, se.tdmax);
         const double k1 = se.k[0], k2 = se.k[1], k3 = se.k[2], k4 = se.k[3];
         double th = fmin(tdc, (double)se.theta_max);
@@ -90,239 +131,447 @@ __global__ void __launch_bounds__(1024) k_render_camera(
         if (td > 0.0) { cp = mx / td; sp = my / td; }
         double st, ct;
         sincos(th, &st, &ct);
-        split_hilo(st * cp, dhx, dlx);
-        split_hilo(st * sp, dhy, dly);
-        split_hilo(ct, dhz, dlz);
+        split_hilo(st * cp, ry.dh[0], ry.dl[0]);
+        split_hilo(st * sp, ry.dh[1], ry.dl[1]);
+        split_hilo(ct, ry.dh[2], ry.dl[2]);
     }
-
-    uint2 rg = ranges[tile];
-    if (d_overflow && *d_overflow) rg.y = rg.x;
-    const uint32_t start = rg.x, end = rg.y;
-
-    float T = 1.f, A = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
-    bool done = !valid;
-    const float near_p = op.near_plane, amax = op.alpha_max, amin = op.alpha_min, tmin = op.t_min,
-                sup = op.support, inv_s2 = op.inv_sigma2;
-
-    const uint32_t total = end - start;
-    const uint32_t nb = (total + B - 1) / B;
-    if (nb > 0) stage_batch<R4>(smem, rec, values, start, min((uint32_t)B, total));
-    for (uint32_t b = 0; b < nb; ++b) {
-        if (b + 1 < nb) {
-            const uint32_t f = start + (b + 1) * B;
-            stage_batch<R4>(smem + ((b + 1) & 1) * B * R4, rec, values, f, min((uint32_t)B, end - f));
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const float4 *buf = smem + (b & 1) * B * R4;
-        const int cnt = (int)min((uint32_t)B, end - (start + b * B));
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                const float4 *r = buf + j * R4;
-                float rho3, rho2, ir, dep3, depc, o;
-                bool keep;
-                if (KIND == GS_PINHOLE) {
-                    const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3];
-                    const float dx = (px - g2.x) - g2.z, dy = (py - g2.y) - g2.w;
-                    const float q0 = fmaf(g0.x, dx, g0.y * dy);
-                    const float q1 = fmaf(g0.z, dx, g0.w * dy);
-                    const float q2 = fmaf(g1.x, dx, fmaf(g1.y, dy, g1.z));
-                    const float n3 = fmaf(q0, q0, q1 * q1);
-                    const float s2 = fmaf(dx, dx, dy * dy);
-                    keep = !(n3 > g1.w * q2 * q2) || !(s2 > g3.x);
-                    if (!keep) continue;
-                    ir = fast_rcp(q2);
-                    rho3 = n3 * ir * ir;
-                    rho2 = s2 * inv_s2;
-                    dep3 = g3.z * ir;
-                    depc = g3.w;
-                    o = g3.y;
-                } else {
-                    const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3], g4 = r[4], g5 = r[5], g6 = r[6];
-                    const float ex = (dhx - g0.x) + (dlx - g1.x);
-                    const float ey = (dhy - g0.y) + (dly - g1.y);
-                    const float ez = (dhz - g0.z) + (dlz - g1.z);
-                    const float hu = fmaf(g2.x, ex, fmaf(g2.y, ey, g2.z * ez));
-                    const float hv = fmaf(g3.x, ex, fmaf(g3.y, ey, g3.z * ez));
-                    const float Dd = fmaf(g4.x, ex, fmaf(g4.y, ey, fmaf(g4.z, ez, g1.w)));
-                    const float n3 = fmaf(hu, hu, hv * hv);
-                    const float dx = (px - g5.x) - g5.z, dy = (py - g5.y) - g5.w;
-                    const float s2 = fmaf(dx, dx, dy * dy);
-                    keep = !(n3 > g0.w * Dd * Dd) || !(s2 > g6.x);
-                    if (!keep) continue;
-                    ir = fast_rcp(Dd);
-                    rho3 = n3 * ir * ir;
-                    rho2 = s2 * inv_s2;
-                    dep3 = g3.w * ir;
-                    depc = g4.w;
-                    o = g2.w;
-                }
-                const bool use3 = rho3 <= rho2;
-                const float rho = use3 ? rho3 : rho2;
-                const float dep = use3 ? dep3 : depc;
-                if (!(rho <= sup) || !(dep >= near_p)) continue;
-                const float a = fminf(amax, o * fast_ex2(-LOG2E_HALF * rho));
-                if (!(a >= amin)) continue;
-                const float Tn = T * (1.f - a);
-                if (Tn < tmin) { done = true; break; }
-                const float w = a * T;
-                float4 c0, c1;
-                if (KIND == GS_PINHOLE) { c0 = r[4]; c1 = r[5]; }
-                else { c0 = r[7]; c1 = r[8]; }
-                C0 = fmaf(w, c0.x, C0); C1 = fmaf(w, c0.y, C1); C2 = fmaf(w, c0.z, C2);
-                N0 = fmaf(w, c0.w, N0); N1 = fmaf(w, c1.x, N1); N2 = fmaf(w, c1.y, N2);
-                D = fmaf(w, dep, D);
-                A += w;
-                T = Tn;
-            }
-        }
-        if (__syncthreads_count(!done) == 0) break;
-    }
-    if (!inside) return;
-    const size_t HW = (size_t)se.width * se.height, pix = (size_t)pyi * se.width + pxi;
-    if (!valid) {
-        if (out_rgb) { out_rgb[pix] = op.bg[0]; out_rgb[HW + pix] = op.bg[1]; out_rgb[2 * HW + pix] = op.bg[2]; }
-        if (out_depth) out_depth[pix] = 0.f;
-        if (out_normal) { out_normal[pix] = 0.f; out_normal[HW + pix] = 0.f; out_normal[2 * HW + pix] = 0.f; }
-        out_alpha[pix] = 0.f;
-        return;
-    }
-    if (out_rgb) {
-        out_rgb[pix] = fmaf(T, op.bg[0], C0);
-        out_rgb[HW + pix] = fmaf(T, op.bg[1], C1);
-        out_rgb[2 * HW + pix] = fmaf(T, op.bg[2], C2);
-    }
-    if (out_depth) out_depth[pix] = A > 0.f ? D / A : 0.f;
-    if (out_normal) { out_normal[pix] = N0; out_normal[HW + pix] = N1; out_normal[2 * HW + pix] = N2; }
-    out_alpha[pix] = A;
-}
-
-// ------------------------------------------------------------------ LiDAR
-__global__ void __launch_bounds__(1024) k_render_lidar(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
-    const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
-    const __grid_constant__ DevSensor se, const DevOpts op, float *__restrict__ out_range,
-    float *__restrict__ out_int, float *__restrict__ out_drop, float *__restrict__ out_alpha) {
-    constexpr int R4 = LI_FLOATS / 4;
-    extern __shared__ float4 smem[];
-    const int B = blockDim.x;
-    const int tile = blockIdx.x;
-    const int tyi = tile / se.ntx, txi = tile - tyi * se.ntx;
-    const int lx = threadIdx.x % se.tw, ly = threadIdx.x / se.tw;
-    const int col = txi * se.tw + lx, row = tyi * se.th + ly;
-    const bool inside = (ly < se.th) && col < se.width && row < se.height;
-
-    float dhx = 0.f, dhy = 0.f, dhz = 0.f, dlx = 0.f, dly = 0.f, dlz = 0.f;
-    if (inside) {   // Eq. 5 ray in fp64: theta = elevation (row), phi = azimuth (column)
-        const double th = (double)se.beam[row];
-        const double ph = (double)se.az0 + (double)col * (double)se.az_step;
+    if (KIND == GS_LIDAR_SPINNING && ry.inside) {   // Eq. 5: theta = elevation (row), phi = azimuth (column)
+        const double th = (double)se.beam[ry.pyi];
+        const double ph = (double)se.az0 + (double)ry.pxi * (double)se.az_step;
         double st, ct, sf, cf;
         sincos(th, &st, &ct);
         sincos(ph, &sf, &cf);
-        split_hilo(ct * cf, dhx, dlx);
-        split_hilo(ct * sf, dhy, dly);
-        split_hilo(st, dhz, dlz);
+        split_hilo(ct * cf, ry.dh[0], ry.dl[0]);
+        split_hilo(ct * sf, ry.dh[1], ry.dl[1]);
+        split_hilo(st, ry.dh[2], ry.dl[2]);
     }
-    uint2 rg = ranges[tile];
-    if (d_overflow && *d_overflow) rg.y = rg.x;
-    const uint32_t start = rg.x, end = rg.y;
-    float T = 1.f, A = 0.f, Rg = 0.f, I = 0.f, Pd = 0.f;
-    bool done = !inside;
-    const float near_p = op.near_plane, amax = op.alpha_max, amin = op.alpha_min, tmin = op.t_min,
-                sup = op.support;
-    const uint32_t total = end - start;
-    const uint32_t nb = (total + B - 1) / B;
-    if (nb > 0) stage_batch<R4>(smem, rec, values, start, min((uint32_t)B, total));
+    return ry;
+}
+
+__device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int x, int xw, int y) {
+    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+    const uint32_t wx = (uint32_t)(x1 - x0);
+    const bool okx = (uint32_t)(x - x0) <= wx || (uint32_t)(xw - x0) <= wx;
+    return okx && (uint32_t)(y - y0) <= (uint32_t)(y1 - y0);
+}
+
+// One (sample, surfel) evaluation in list order.  Returns false once the ray
+// stops (the surfel that would push T below t_min is not composited, R3).
+template <int KIND, bool STATS>
+__device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const Ray &ry, const DevOpts &op,
+                                            Acc &a, uint32_t &n_eval, uint32_t &n_comp) {
+    if (STATS) {
+        constexpr int BB4 = Rec<KIND>::BB / 4;
+        const float4 bb = r[BB4];
+        if (in_box(__float_as_uint(bb.z), __float_as_uint(bb.w), ry.pxi, ry.pxw, ry.pyi)) ++n_eval;
+    }
+    float rho3, rho2, ir, dep3, depc, o;
+    if (KIND == GS_PINHOLE) {
+        const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3];
+        const float dx = (ry.px - g2.x) - g2.z, dy = (ry.py - g2.y) - g2.w;
+        const float q0 = fmaf(g0.x, dx, g0.y * dy);
+        const float q1 = fmaf(g0.z, dx, g0.w * dy);
+        const float q2 = fmaf(g1.x, dx, fmaf(g1.y, dy, g1.z));
+        const float n3 = fmaf(q0, q0, q1 * q1);
+        const float s2 = fmaf(dx, dx, dy * dy);
+        if ((n3 > g1.w * q2 * q2) && (s2 > g3.x)) return true;
+        ir = fast_rcp(q2);
+        rho3 = n3 * ir * ir;
+        rho2 = s2 * op.inv_sigma2;
+        dep3 = g3.z * ir;
+        depc = g3.w;
+        o = g3.y;
+    } else {
+        const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3], g4 = r[4];
+        const float ex = (ry.dh[0] - g0.x) + (ry.dl[0] - g1.x);
+        const float ey = (ry.dh[1] - g0.y) + (ry.dl[1] - g1.y);
+        const float ez = (ry.dh[2] - g0.z) + (ry.dl[2] - g1.z);
+        const float hu = fmaf(g2.x, ex, fmaf(g2.y, ey, g2.z * ez));
+        const float hv = fmaf(g3.x, ex, fmaf(g3.y, ey, g3.z * ez));
+        const float Dd = fmaf(g4.x, ex, fmaf(g4.y, ey, fmaf(g4.z, ez, g1.w)));
+        const float n3 = fmaf(hu, hu, hv * hv);
+        if (KIND == GS_FISHEYE_EQUIDISTANT) {
+            const float4 g5 = r[5], g6 = r[6];
+            const float dx = (ry.px - g5.x) - g5.z, dy = (ry.py - g5.y) - g5.w;
+            const float s2 = fmaf(dx, dx, dy * dy);
+            if ((n3 > g0.w * Dd * Dd) && (s2 > g6.x)) return true;
+            rho2 = s2 * op.inv_sigma2;
+        } else {
+            if (n3 > g0.w * Dd * Dd) return true;
+            rho2 = __int_as_float(0x7f800000);   // no low-pass for LiDAR (R6)
+        }
+        ir = fast_rcp(Dd);
+        rho3 = n3 * ir * ir;
+        dep3 = g3.w * ir;
+        depc = g4.w;
+        o = g2.w;
+    }
+    const bool use3 = rho3 <= rho2;
+    const float rho = use3 ? rho3 : rho2;
+    const float dep = use3 ? dep3 : depc;
+    if (!(rho <= op.support) || !(dep >= op.near_plane)) return true;
+    const float al = fminf(op.alpha_max, o * fast_ex2(-LOG2E_HALF * rho));
+    if (!(al >= op.alpha_min)) return true;
+    const float Tn = a.T * (1.f - al);
+    if (Tn < op.t_min) return false;
+    const float w = al * a.T;
+    if (KIND == GS_LIDAR_SPINNING) {
+        const float4 p = r[5];
+        a.c0 = fmaf(w, p.x, a.c0);   // intensity
+        a.c1 = fmaf(w, p.y, a.c1);   // ray-drop probability
+    } else {
+        float4 c0, c1;
+        if (KIND == GS_PINHOLE) { c0 = r[4]; c1 = r[5]; } else { c0 = r[7]; c1 = r[8]; }
+        a.c0 = fmaf(w, c0.x, a.c0); a.c1 = fmaf(w, c0.y, a.c1); a.c2 = fmaf(w, c0.z, a.c2);
+        a.n0 = fmaf(w, c0.w, a.n0); a.n1 = fmaf(w, c1.x, a.n1); a.n2 = fmaf(w, c1.y, a.n2);
+    }
+    a.d = fmaf(w, dep, a.d);
+    a.A += w;
+    a.T = Tn;
+    if (STATS) ++n_comp;
+    return true;
+}
+
+// Walk list entries [s, e) of `values` for the 32 lanes of this warp.
+// wbuf: warp-private shared memory, 2 x 32 records.  `done` lanes skip work;
+// a lane becomes done when its ray stops.  Returns true if the ray stopped.
+template <int KIND, bool STATS>
+__device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+                                     uint32_t s, uint32_t e, float4 *wbuf, const Ray &ry,
+                                     const DevOpts &op, Acc &a, bool &done, bool &stopped,
+                                     uint32_t &n_eval, uint32_t &n_comp) {
+    constexpr int R4 = Rec<KIND>::F / 4;
+    const int lane = threadIdx.x & 31;
+    if (__all_sync(0xffffffffu, done) || s >= e) return;
+    auto stage = [&](uint32_t first, float4 *dst) {
+        if (first + lane < e) {
+            const uint32_t id = __ldg(values + first + lane);
+            const float4 *src = rec + (size_t)id * R4;
+            float4 *d = dst + lane * R4;
+#pragma unroll
+            for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
+        }
+        cp_async_commit();
+    };
+    const uint32_t nb = (e - s + 31) >> 5;
+    stage(s, wbuf);
     for (uint32_t b = 0; b < nb; ++b) {
         if (b + 1 < nb) {
-            const uint32_t f = start + (b + 1) * B;
-            stage_batch<R4>(smem + ((b + 1) & 1) * B * R4, rec, values, f, min((uint32_t)B, end - f));
+            stage(s + (b + 1) * 32, wbuf + ((b + 1) & 1) * 32 * R4);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
-        const float4 *buf = smem + (b & 1) * B * R4;
-        const int cnt = (int)min((uint32_t)B, end - (start + b * B));
+        __syncwarp();
+        const float4 *buf = wbuf + (b & 1) * 32 * R4;
+        const int cnt = (int)min(32u, e - (s + b * 32));
         if (!done) {
             for (int j = 0; j < cnt; ++j) {
-                const float4 *r = buf + j * R4;
-                const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3], g4 = r[4];
-                const float ex = (dhx - g0.x) + (dlx - g1.x);
-                const float ey = (dhy - g0.y) + (dly - g1.y);
-                const float ez = (dhz - g0.z) + (dlz - g1.z);
-                const float hu = fmaf(g2.x, ex, fmaf(g2.y, ey, g2.z * ez));
-                const float hv = fmaf(g3.x, ex, fmaf(g3.y, ey, g3.z * ez));
-                const float Dd = fmaf(g4.x, ex, fmaf(g4.y, ey, fmaf(g4.z, ez, g1.w)));
-                const float n3 = fmaf(hu, hu, hv * hv);
-                if (n3 > g0.w * Dd * Dd) continue;
-                const float ir = fast_rcp(Dd);
-                const float rho = n3 * ir * ir;
-                const float t = g3.w * ir;
-                if (!(rho <= sup) || !(t >= near_p)) continue;
-                const float a = fminf(amax, g2.w * fast_ex2(-LOG2E_HALF * rho));
-                if (!(a >= amin)) continue;
-                const float Tn = T * (1.f - a);
-                if (Tn < tmin) { done = true; break; }
-                const float w = a * T;
-                const float4 p = r[5];
-                Rg = fmaf(w, t, Rg);
-                I = fmaf(w, p.x, I);
-                Pd = fmaf(w, p.y, Pd);
-                A += w;
-                T = Tn;
+                if (!eval_record<KIND, STATS>(buf + j * R4, ry, op, a, n_eval, n_comp)) {
+                    done = true;
+                    stopped = true;
+                    break;
+                }
             }
         }
-        if (__syncthreads_count(!done) == 0) break;
+        if (__all_sync(0xffffffffu, done)) {
+            cp_async_wait<0>();
+            __syncwarp();
+            return;
+        }
+        __syncwarp();
     }
-    if (!inside) return;
-    const size_t pix = (size_t)row * se.width + col;
-    if (out_range) out_range[pix] = A > 0.f ? Rg / A : op.bg_range;
-    if (out_int) out_int[pix] = I;
-    if (out_drop) out_drop[pix] = fmaf(T, op.bg_raydrop, Pd);
-    out_alpha[pix] = A;
 }
 
-// ------------------------------------------------------------------ host
+template <int KIND>
+__device__ __forceinline__ void write_final(const DevSensor &se, const DevOpts &op, const Ray &ry,
+                                            const Acc &a, float *o0, float *o1, float *o2, float *o3) {
+    if (!ry.inside) return;
+    const size_t HW = (size_t)se.width * se.height, pix = (size_t)ry.pyi * se.width + ry.pxi;
+    if (KIND == GS_LIDAR_SPINNING) {   // o0 range, o1 intensity, o2 raydrop, o3 alpha
+        if (o0) o0[pix] = a.A > 0.f ? a.d / a.A : op.bg_range;
+        if (o1) o1[pix] = a.c0;
+        if (o2) o2[pix] = fmaf(a.T, op.bg_raydrop, a.c1);
+        o3[pix] = a.A;
+        return;
+    }
+    // cameras: o0 rgb [3,H,W], o1 depth, o2 normal [3,H,W], o3 alpha
+    if (!ry.valid) {
+        if (o0) { o0[pix] = op.bg[0]; o0[HW + pix] = op.bg[1]; o0[2 * HW + pix] = op.bg[2]; }
+        if (o1) o1[pix] = 0.f;
+        if (o2) { o2[pix] = 0.f; o2[HW + pix] = 0.f; o2[2 * HW + pix] = 0.f; }
+        o3[pix] = 0.f;
+        return;
+    }
+    if (o0) {
+        o0[pix] = fmaf(a.T, op.bg[0], a.c0);
+        o0[HW + pix] = fmaf(a.T, op.bg[1], a.c1);
+        o0[2 * HW + pix] = fmaf(a.T, op.bg[2], a.c2);
+    }
+    if (o1) o1[pix] = a.A > 0.f ? a.d / a.A : 0.f;
+    if (o2) { o2[pix] = a.n0; o2[HW + pix] = a.n1; o2[2 * HW + pix] = a.n2; }
+    o3[pix] = a.A;
+}
+
+__device__ __forceinline__ uint32_t seg_count(uint32_t len, uint32_t L) { return len <= L ? 1u : (len + L - 1) / L; }
+__device__ __forceinline__ uint32_t bucket_of(uint32_t len, uint32_t L) {
+    if (len == 0) return 0;
+    const uint32_t b = 32 - __clz(min(len, L));
+    return b >= NB ? NB - 1 : b;
+}
+
+// ---------------------------------------------------------------- schedule
+__global__ void k_sched_count(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow,
+                              SchedHdr *h, uint32_t L) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const bool ovf = d_overflow && *d_overflow;
+    const uint2 rg = ranges[t];
+    const uint32_t len = ovf ? 0u : rg.y - rg.x;
+    atomicAdd(&h->bucket_cnt[bucket_of(len, L)], seg_count(len, L));
+}
+
+__global__ void k_sched_scan(SchedHdr *h) {   // one warp: descending-bucket exclusive scan
+    const int lane = threadIdx.x;
+    const uint32_t c = h->bucket_cnt[NB - 1 - lane];
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    h->bucket_cur[NB - 1 - lane] = x - c;
+    if (lane == 31) h->n_items = x;
+}
+
+__global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow,
+                             SchedHdr *h, uint2 *__restrict__ items, uint32_t *__restrict__ split_base,
+                             uint32_t *__restrict__ split_list, uint32_t L) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const bool ovf = d_overflow && *d_overflow;
+    const uint2 rg = ranges[t];
+    const uint32_t len = ovf ? 0u : rg.y - rg.x;
+    const uint32_t ns = seg_count(len, L);
+    const uint32_t pos = atomicAdd(&h->bucket_cur[bucket_of(len, L)], ns);
+    for (uint32_t k = 0; k < ns; ++k) items[pos + k] = make_uint2((uint32_t)t, k);
+    if (ns > 1) {
+        split_base[t] = atomicAdd(&h->slot_cursor, ns);
+        split_list[atomicAdd(&h->n_split, 1u)] = (uint32_t)t;
+    }
+}
+
+// ---------------------------------------------------------------- composite
+template <int KIND, bool STATS>
+__global__ void __launch_bounds__(WARPS * 32) k_render(
+    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
+    const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
+    const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
+    float *__restrict__ partials, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t L) {
+    constexpr int R4 = Rec<KIND>::F / 4;
+    extern __shared__ float4 smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float4 *wbuf = smem + warp * 2 * 32 * R4;
+    const bool ovf = d_overflow && *d_overflow;
+    const uint32_t n_items = h->n_items;
+    while (true) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(&h->counter, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const uint2 it = items[item];
+        const int tile = (int)it.x;
+        const uint32_t seg = it.y;
+        uint2 rg = ranges[tile];
+        if (ovf) rg.y = rg.x;
+        const uint32_t len = rg.y - rg.x, ns = seg_count(len, L);
+        const uint32_t s = rg.x + seg * L, e = min(rg.y, s + L);
+        const Ray ry = make_ray<KIND>(se, tile, lane);
+        Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bool done = !ry.valid, stopped = false;
+        uint32_t n_eval = 0, n_comp = 0;
+        walk<KIND, STATS>(rec, values, s, e, wbuf, ry, op, a, done, stopped, n_eval, n_comp);
+        if (ns == 1) {
+            write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
+            if (STATS && ry.inside) {
+                const size_t HW = (size_t)se.width * se.height, pix = (size_t)ry.pyi * se.width + ry.pxi;
+                out_stats[pix] = n_comp;
+                out_stats[HW + pix] = n_eval;
+            }
+        } else {
+            float *p = partials + ((size_t)(split_base[tile] + seg) * 32 + lane) * NPART;
+            p[0] = a.T; p[1] = a.A; p[2] = a.c0; p[3] = a.c1; p[4] = a.c2;
+            p[5] = a.d; p[6] = a.n0; p[7] = a.n1; p[8] = a.n2; p[9] = stopped ? 1.f : 0.f;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- merge of split lists
+// One CTA per split tile.  Warp 0 walks the segment composites in order,
+// C += T_run C_k, T_run *= T_k, while no stop can have happened
+// (no local stop and T_run T_k >= t_min); the first segment in which a ray
+// stops with T_run < 1 is re-walked from T_run with the exact stop rule (the
+// 8 warps share the distinct re-walk segments).
+template <int KIND>
+__global__ void __launch_bounds__(WARPS * 32) k_merge(
+    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
+    const SchedHdr *h, const uint32_t *__restrict__ split_base, const uint32_t *__restrict__ split_list,
+    const float *__restrict__ partials, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t L) {
+    constexpr int R4 = Rec<KIND>::F / 4;
+    extern __shared__ float4 smem[];
+    __shared__ int s_k[32];
+    __shared__ float s_T[32];
+    __shared__ Acc s_acc[32], s_re[32];
+    if (blockIdx.x >= h->n_split) return;
+    const int tile = (int)split_list[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint2 rg = ranges[tile];
+    const uint32_t ns = seg_count(rg.y - rg.x, L), base = split_base[tile];
+    const Ray ry = make_ray<KIND>(se, tile, lane);
+    if (warp == 0) {
+        Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int kstar = -1;
+        for (uint32_t k = 0; k < ns; ++k) {
+            const float *p = partials + ((size_t)(base + k) * 32 + lane) * NPART;
+            const float Tk = p[0];
+            const bool stop_k = p[9] != 0.f;
+            if (!stop_k && a.T * Tk >= op.t_min) {
+                const float Tr = a.T;
+                a.A = fmaf(Tr, p[1], a.A); a.c0 = fmaf(Tr, p[2], a.c0); a.c1 = fmaf(Tr, p[3], a.c1);
+                a.c2 = fmaf(Tr, p[4], a.c2); a.d = fmaf(Tr, p[5], a.d); a.n0 = fmaf(Tr, p[6], a.n0);
+                a.n1 = fmaf(Tr, p[7], a.n1); a.n2 = fmaf(Tr, p[8], a.n2);
+                a.T = Tr * Tk;
+            } else if (a.T == 1.f) {   // nothing composited before: the local composite is exact
+                a.T = Tk; a.A = p[1]; a.c0 = p[2]; a.c1 = p[3]; a.c2 = p[4];
+                a.d = p[5]; a.n0 = p[6]; a.n1 = p[7]; a.n2 = p[8];
+                break;
+            } else {
+                kstar = (int)k;
+                break;
+            }
+        }
+        s_k[lane] = ry.valid ? kstar : -1;
+        s_T[lane] = a.T;
+        s_acc[lane] = a;
+        s_re[lane] = Acc{a.T, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    }
+    __syncthreads();
+    // distinct re-walk segments, dealt round-robin to the warps
+    int nd = 0;
+    for (int i = 0; i < 32; ++i) {
+        const int k = s_k[i];
+        if (k < 0) continue;
+        bool first = true;
+        for (int j = 0; j < i; ++j) first = first && (s_k[j] != k);
+        if (!first) continue;
+        if (nd % WARPS == warp) {
+            const bool mine = s_k[lane] == k;
+            Acc a = {s_T[lane], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            bool done = !mine, stopped = false;
+            uint32_t ne = 0, nc = 0;
+            const uint32_t s = rg.x + (uint32_t)k * L, e = min(rg.y, s + L);
+            walk<KIND, false>(rec, values, s, e, smem + warp * 2 * 32 * R4, ry, op, a, done, stopped, ne, nc);
+            if (mine) s_re[lane] = a;
+        }
+        ++nd;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        Acc a = s_acc[lane];
+        const Acc r = s_re[lane];
+        if (s_k[lane] >= 0) {
+            a.T = r.T; a.A += r.A; a.c0 += r.c0; a.c1 += r.c1; a.c2 += r.c2;
+            a.d += r.d; a.n0 += r.n0; a.n1 += r.n1; a.n2 += r.n2;
+        }
+        write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
+    }
+}
+
+// ---------------------------------------------------------------- host
+size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len) {
+    return RenderWs(cap, ntiles, split_len).total;
+}
+
+template <int KIND, bool STATS>
+static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, const uint32_t *ranges,
+                          const int32_t *d_overflow, const DevSensor &se, const DevOpts &op, int32_t split_len,
+                          void *ws, size_t ws_bytes, float *o0, float *o1, float *o2, float *o3,
+                          uint32_t *stats, cudaStream_t st) {
+    const ProjLayout PL(n, se.kind);
+    const float4 *rec = (const float4 *)((const char *)proj + PL.rec);
+    const int ntiles = se.ntx * se.nty;
+    // capacity implied by the workspace size (the pair capacity of gs_bin_sort)
+    int64_t cap = 0;
+    {
+        int64_t lo = 0, hi = (int64_t)1 << 31;
+        while (lo < hi) {   // largest cap whose layout fits
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (RenderWs(mid, ntiles, split_len).total <= ws_bytes) lo = mid; else hi = mid - 1;
+        }
+        cap = lo;
+    }
+    const RenderWs W(cap, ntiles, split_len);
+    char *wb = (char *)ws;
+    SchedHdr *h = (SchedHdr *)(wb + W.hdr);
+    uint2 *items = (uint2 *)(wb + W.items);
+    uint32_t *split_base = (uint32_t *)(wb + W.split_base), *split_list = (uint32_t *)(wb + W.split_list);
+    float *partials = (float *)(wb + W.partials);
+    const uint32_t L = STATS ? 0x7fffffffu : W.L;   // instrumented runs are never split
+    cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
+    if (e != cudaSuccess) return e;
+    const unsigned gt = (unsigned)((ntiles + 255) / 256);
+    k_sched_count<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, L);
+    k_sched_scan<<<1, 32, 0, st>>>(h);
+    k_sched_fill<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, items, split_base, split_list, L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    constexpr int R4 = Rec<KIND>::F / 4;
+    const size_t sm = (size_t)WARPS * 2 * 32 * R4 * 16;
+    e = cudaFuncSetAttribute(k_render<KIND, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, WARPS * 32, sm);
+    const unsigned grid = (unsigned)std::max(1, std::min(nsm * std::max(per, 1), (ntiles + WARPS - 1) / WARPS + nsm));
+    k_render<KIND, STATS><<<grid, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
+                                                        items, split_base, partials, o0, o1, o2, o3, stats, L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (!STATS && W.max_split > 0) {
+        e = cudaFuncSetAttribute(k_merge<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        k_merge<KIND><<<W.max_split, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_base,
+                                                           split_list, partials, o0, o1, o2, o3, L);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
 cudaError_t launch_render_camera(const void *proj, int64_t n, const uint32_t *values,
                                  const uint32_t *ranges, const int32_t *d_overflow,
-                                 const DevSensor &se, const DevOpts &op, float *rgb, float *depth,
-                                 float *normal, float *alpha, cudaStream_t st) {
-    const ProjLayout L(n, se.kind);
-    const float4 *rec = (const float4 *)((const char *)proj + L.rec);
-    const int B = se.tw * se.th;
-    const unsigned grid = (unsigned)(se.ntx * se.nty);
-    if (se.kind == GS_PINHOLE) {
-        const size_t sm = 2 * (size_t)B * PH_FLOATS * 4;
-        cudaFuncSetAttribute(k_render_camera<GS_PINHOLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_render_camera<GS_PINHOLE><<<grid, B, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op,
-                                                         rgb, depth, normal, alpha);
-    } else {
-        const size_t sm = 2 * (size_t)B * FE_FLOATS * 4;
-        cudaFuncSetAttribute(k_render_camera<GS_FISHEYE_EQUIDISTANT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
-        k_render_camera<GS_FISHEYE_EQUIDISTANT><<<grid, B, sm, st>>>(rec, values, (const uint2 *)ranges,
-                                                                     d_overflow, se, op, rgb, depth, normal,
-                                                                     alpha);
-    }
-    return cudaGetLastError();
+                                 const DevSensor &se, const DevOpts &op, int32_t split_len, void *ws,
+                                 size_t ws_bytes, float *rgb, float *depth, float *normal, float *alpha,
+                                 uint32_t *stats, cudaStream_t st) {
+    if (se.kind == GS_PINHOLE)
+        return stats ? launch<GS_PINHOLE, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st)
+                     : launch<GS_PINHOLE, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st);
+    return stats ? launch<GS_FISHEYE_EQUIDISTANT, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st)
+                 : launch<GS_FISHEYE_EQUIDISTANT, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st);
 }
 
 cudaError_t launch_render_lidar(const void *proj, int64_t n, const uint32_t *values,
                                 const uint32_t *ranges, const int32_t *d_overflow,
-                                const DevSensor &se, const DevOpts &op, float *range, float *inten,
-                                float *drop, float *alpha, cudaStream_t st) {
-    const ProjLayout L(n, se.kind);
-    const float4 *rec = (const float4 *)((const char *)proj + L.rec);
-    const int B = se.tw * se.th;
-    const unsigned grid = (unsigned)(se.ntx * se.nty);
-    const size_t sm = 2 * (size_t)B * LI_FLOATS * 4;
-    cudaFuncSetAttribute(k_render_lidar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_render_lidar<<<grid, B, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, range, inten,
-                                        drop, alpha);
-    return cudaGetLastError();
+                                const DevSensor &se, const DevOpts &op, int32_t split_len, void *ws,
+                                size_t ws_bytes, float *range, float *inten, float *drop, float *alpha,
+                                uint32_t *stats, cudaStream_t st) {
+    return stats ? launch<GS_LIDAR_SPINNING, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, range, inten, drop, alpha, stats, st)
+                 : launch<GS_LIDAR_SPINNING, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, range, inten, drop, alpha, stats, st);
 }
 
 }  // namespace gsr

@@ -43,7 +43,8 @@ class gs_sensor(C.Structure):
 
 
 class gs_opts(C.Structure):
-    _fields_ = [("tile_w", C.c_int32), ("tile_h", C.c_int32), ("near_plane", C.c_float),
+    _fields_ = [("tile_w", C.c_int32), ("tile_h", C.c_int32), ("split_len", C.c_int32),
+                ("near_plane", C.c_float),
                 ("alpha_max", C.c_float), ("alpha_min", C.c_float), ("t_min", C.c_float),
                 ("support_rho", C.c_float), ("lowpass_sigma_px", C.c_float),
                 ("bg_rgb", C.c_float * 3), ("bg_range", C.c_float), ("bg_raydrop", C.c_float)]
@@ -51,7 +52,7 @@ class gs_opts(C.Structure):
 
 EXPORTS = ["gs_default_opts", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
-           "gs_status_string", "gs_last_error", "gs_record_bytes"]
+           "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes"]
 
 _lib = None
 
@@ -83,11 +84,13 @@ def load(build_if_missing: bool = True):
     lib.gs_bin_sort.argtypes = [vp, C.c_int64, P(gs_sensor), P(gs_opts), vp, vp, C.c_int64, vp, vp,
                                 C.c_size_t, vp, vp]
     lib.gs_bin_sort.restype = C.c_int
-    lib.gs_render_camera.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp, vp, vp,
-                                     vp, vp]
+    lib.gs_render_workspace_bytes.argtypes = [C.c_int64, P(gs_sensor), P(gs_opts)]
+    lib.gs_render_workspace_bytes.restype = C.c_size_t
+    lib.gs_render_camera.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp,
+                                     C.c_size_t, vp, vp, vp, vp, vp, vp]
     lib.gs_render_camera.restype = C.c_int
-    lib.gs_render_lidar.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp, vp, vp,
-                                    vp, vp]
+    lib.gs_render_lidar.argtypes = [vp, C.c_int64, vp, vp, vp, P(gs_sensor), P(gs_opts), vp,
+                                    C.c_size_t, vp, vp, vp, vp, vp, vp]
     lib.gs_render_lidar.restype = C.c_int
     lib.gs_projected_offsets.argtypes = [C.c_int64, C.c_int32, vp]
     lib.gs_projected_offsets.restype = None
@@ -196,15 +199,23 @@ def gs_bin_sort(projected, n, sensor: Sensor, opts: gs_opts, keys, values, cap, 
                               C.c_void_p(stream)))
 
 
+def gs_render_workspace_bytes(cap, sensor: Sensor, opts: gs_opts):
+    return int(load().gs_render_workspace_bytes(int(cap), sensor.ref, C.byref(opts)))
+
+
 def gs_render_camera(projected, n, values, tile_ranges, d_overflow, sensor: Sensor, opts: gs_opts,
-                     rgb, depth, normal, alpha, stream):
+                     workspace, rgb, depth, normal, alpha, stream, stats=None):
     _check(load().gs_render_camera(_ptr(projected), int(n), _ptr(values), _ptr(tile_ranges),
-                                   _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(rgb),
-                                   _ptr(depth), _ptr(normal), _ptr(alpha), C.c_void_p(stream)))
+                                   _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(workspace),
+                                   workspace.numel() * workspace.element_size(), _ptr(rgb),
+                                   _ptr(depth), _ptr(normal), _ptr(alpha), _ptr(stats),
+                                   C.c_void_p(stream)))
 
 
 def gs_render_lidar(projected, n, values, tile_ranges, d_overflow, sensor: Sensor, opts: gs_opts,
-                    rng, intensity, raydrop, alpha, stream):
+                    workspace, rng, intensity, raydrop, alpha, stream, stats=None):
     _check(load().gs_render_lidar(_ptr(projected), int(n), _ptr(values), _ptr(tile_ranges),
-                                  _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(rng),
-                                  _ptr(intensity), _ptr(raydrop), _ptr(alpha), C.c_void_p(stream)))
+                                  _ptr(d_overflow), sensor.ref, C.byref(opts), _ptr(workspace),
+                                  workspace.numel() * workspace.element_size(), _ptr(rng),
+                                  _ptr(intensity), _ptr(raydrop), _ptr(alpha), _ptr(stats),
+                                  C.c_void_p(stream)))

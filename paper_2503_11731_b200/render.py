@@ -35,12 +35,19 @@ def n_channels(kind):
 
 
 class Renderer:
-    def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda"):
+    def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda",
+                 lidar_tile=(32, 1)):
+        """opts apply to every frame; LiDAR frames use `lidar_tile` (columns x
+        beams of one warp-tile) unless it is None."""
         self.device = torch.device(device)
         self.t = surfels
         self.n = int(surfels["means"].shape[0])
         self.struct = gsr.surfels_struct(surfels)
-        self.opts = opts if opts is not None else gsr.default_opts()
+        self.cam_opts = opts if opts is not None else gsr.default_opts()
+        self.lidar_opts = gsr.gs_opts.from_buffer_copy(self.cam_opts)
+        if lidar_tile is not None:
+            self.lidar_opts.tile_w, self.lidar_opts.tile_h = int(lidar_tile[0]), int(lidar_tile[1])
+        self.opts = self.cam_opts
         self._buf = {}
         self.last_pairs = None
 
@@ -63,14 +70,23 @@ class Renderer:
         return proj, d_np
 
     def render(self, sensor, out: torch.Tensor | None = None, capacity: int | None = None,
-               keys: bool = False, stream=None) -> torch.Tensor:
+               keys: bool = False, stream=None, stats: torch.Tensor | None = None,
+               events=None) -> torch.Tensor:
         """Render one frame; returns a planar fp32 tensor [C,H,W] (C = 8 for
         cameras: r,g,b,depth,nx,ny,nz,alpha; 4 for LiDAR: range, intensity,
-        raydrop, alpha)."""
+        raydrop, alpha).  stats: optional int32 [2,H,W] (composited, evaluated
+        pairs per sample).  events: optional 4 CUDA events recorded before
+        gs_project, gs_bin_sort, the render call and after it."""
         if not isinstance(sensor, gsr.Sensor):
             sensor = gsr.Sensor(sensor)
-        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        self.opts = self.lidar_opts if sensor.kind == gsr.GS_LIDAR_SPINNING else self.cam_opts
+        torch_stream = torch.cuda.current_stream(self.device)
+        st = stream if stream is not None else torch_stream.cuda_stream
+        if events is not None:
+            events[0].record(torch_stream)
         proj, d_np = self.project(sensor, st)
+        if events is not None:
+            events[1].record(torch_stream)
         if capacity is None:
             cap = int(d_np.item())   # exact sizing (one sync)
         else:
@@ -87,12 +103,17 @@ class Renderer:
         H, W = sensor.height, sensor.width
         if out is None:
             out = torch.empty((C, H, W), dtype=torch.float32, device=self.device)
+        rws = self._get("rws", gsr.gs_render_workspace_bytes(cap, sensor, self.opts))
+        if events is not None:
+            events[2].record(torch_stream)
         if sensor.kind == gsr.GS_LIDAR_SPINNING:
-            gsr.gs_render_lidar(proj, self.n, values, ranges, ovf, sensor, self.opts, out[0], out[1],
-                                out[2], out[3], st)
+            gsr.gs_render_lidar(proj, self.n, values, ranges, ovf, sensor, self.opts, rws, out[0],
+                                out[1], out[2], out[3], st, stats)
         else:
-            gsr.gs_render_camera(proj, self.n, values, ranges, ovf, sensor, self.opts, out[0:3],
-                                 out[3], out[4:7], out[7], st)
+            gsr.gs_render_camera(proj, self.n, values, ranges, ovf, sensor, self.opts, rws, out[0:3],
+                                 out[3], out[4:7], out[7], st, stats)
+        if events is not None:
+            events[3].record(torch_stream)
         self._last = dict(proj=proj, values=values, ranges=ranges, overflow=ovf, keys=kbuf, cap=cap,
                           ntiles=nt, sensor=sensor)
         return out

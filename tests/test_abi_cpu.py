@@ -39,7 +39,7 @@ def test_library_is_sm100a_cubin():
 
 def test_default_opts_are_north_star(gsr):
     o = gsr.default_opts()
-    assert (o.tile_w, o.tile_h) == (16, 16)
+    assert (o.tile_w, o.tile_h) == (8, 4) and o.split_len == 0
     assert o.alpha_max == pytest.approx(0.99) and o.alpha_min == pytest.approx(1 / 255)
     assert o.t_min == pytest.approx(1e-4) and o.support_rho == 9.0
     assert o.lowpass_sigma_px == pytest.approx(2 ** -0.5) and o.near_plane == pytest.approx(0.2)
@@ -62,10 +62,13 @@ def test_host_validation_errors(gsr):
     # wrong modality for the call -> configuration error
     li = gsr.Sensor(sg.lidar64(sg.lidar_pose([0, 0, 0]), height=8, width=64))
     dummy = C.c_void_p(1)
-    assert lib.gs_render_camera(dummy, 0, dummy, dummy, None, li.ref, C.byref(opts), None, None,
-                                None, dummy, None) == gsr.GS_ERR_CONFIG
-    assert lib.gs_render_lidar(dummy, 0, dummy, dummy, None, cam.ref, C.byref(opts), None, None,
-                               None, dummy, None) == gsr.GS_ERR_CONFIG
+    assert lib.gs_render_camera(dummy, 0, dummy, dummy, None, li.ref, C.byref(opts), dummy, 1 << 20,
+                                None, None, None, dummy, None, None) == gsr.GS_ERR_CONFIG
+    assert lib.gs_render_lidar(dummy, 0, dummy, dummy, None, cam.ref, C.byref(opts), dummy, 1 << 20,
+                               None, None, None, dummy, None, None) == gsr.GS_ERR_CONFIG
+    # render workspace too small
+    assert lib.gs_render_camera(dummy, 0, dummy, dummy, None, cam.ref, C.byref(opts), dummy, 16,
+                                None, None, None, dummy, None, None) == gsr.GS_ERR_CONFIG
     # non-monotone beam table -> range error
     bad = sg.lidar64(sg.lidar_pose([0, 0, 0]), height=8, width=64)
     bad.beam_elevation = bad.beam_elevation[::-1].copy()
@@ -86,7 +89,8 @@ def test_host_validation_errors(gsr):
 def test_sizes(gsr):
     cam = gsr.Sensor(sg.mid(n=10).sensors[0])
     o = gsr.default_opts()
-    assert gsr.gs_num_tiles(cam, o) == 120 * 68
+    assert gsr.gs_num_tiles(cam, o) == 240 * 270
+    assert gsr.gs_render_workspace_bytes(10_000_000, cam, o) > gsr.gs_render_workspace_bytes(0, cam, o)
     assert gsr.gs_record_bytes(0) == 96 and gsr.gs_record_bytes(1) == 144 and gsr.gs_record_bytes(2) == 96
     offs = gsr.gs_projected_offsets(1000, 0)
     assert offs["total"] == gsr.gs_projected_bytes(1000, 0)

@@ -96,7 +96,7 @@ def test_binning_bit_exact(gsr_mod):
         se = c.sensors[0]
         img, r = _render(c.surfels, se, keys=True)
         b = r.binning_state()
-        ntx = (se.width + 15) // 16
+        ntx = (se.width + r.cam_opts.tile_w - 1) // r.cam_opts.tile_w
         vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
         assert b["P"] == len(vals)
         np.testing.assert_array_equal(b["values"], vals)
@@ -114,7 +114,8 @@ def test_binning_bit_exact_lidar_wrap(gsr_mod):
     se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
     img, r = _render(s, se, keys=True)
     b = r.binning_state()
-    ntx = (se.width + 15) // 16
+    tw = r.lidar_opts.tile_w
+    ntx = (se.width + tw - 1) // tw
     assert np.any(b["rect"][:, 2] >= ntx)   # some surfels straddle the azimuth seam
     vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
     np.testing.assert_array_equal(b["values"], vals)
@@ -122,12 +123,38 @@ def test_binning_bit_exact_lidar_wrap(gsr_mod):
     np.testing.assert_array_equal(b["ranges"], ranges)
 
 
-@pytest.mark.parametrize("tiles", [(8, 8), (32, 8), (16, 4)])
+@pytest.mark.parametrize("tiles", [(4, 8), (16, 2), (32, 1), (5, 5)])
 def test_tile_shape_invariance_bitwise(gsr_mod, tiles):
+    """Unsplit tile lists: per-pair arithmetic never depends on the tile."""
     c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
-    a, _ = _render(c.surfels, c.sensors[0])
-    b, _ = _render(c.surfels, c.sensors[0], opts=dict(tile_w=tiles[0], tile_h=tiles[1]))
+    nosplit = dict(split_len=2 ** 31 - 1)
+    a, _ = _render(c.surfels, c.sensors[0], opts=nosplit)
+    b, _ = _render(c.surfels, c.sensors[0], opts=dict(tile_w=tiles[0], tile_h=tiles[1], **nosplit))
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("cfg", ["street", "fisheye", "lidar"])
+def test_split_lists_match_unsplit_and_oracle(gsr_mod, cfg):
+    """Segmented compositing + transmittance-prefix merge (exact stop rule)
+    agrees with the sequential walk to fp32 rounding and passes the oracle gate."""
+    rng = np.random.default_rng(31)
+    if cfg == "street":
+        c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+        s, se = c.surfels, c.sensors[0]
+    elif cfg == "fisheye":
+        s = sg.street(rng, 30_000, 0.0, 60.0, 3)
+        k, _ = sg.draw_fisheye_k(rng, float(np.float32(np.deg2rad(95))))
+        se = sg.fisheye(176, 136, np.deg2rad(95), k, 88.0, 68.0, sg.camera_pose([0, 1.5, 0], 0.0))
+    else:
+        s = sg.street(rng, 60_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
+        se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
+    a, _ = _render(s, se, opts=dict(split_len=2 ** 31 - 1))
+    b, _ = _render(s, se, opts=dict(split_len=16))
+    assert np.abs(a - b).max() < 2e-5 * max(1.0, np.abs(a).max())
+    rays = np.arange(se.width * se.height)
+    ref, fl, _ = oracle.render(s, se, rays)
+    st = parity.compare(b, ref, fl, rays, se)
+    assert st["ok"], st
 
 
 def test_deterministic_repeat(gsr_mod):
