@@ -1,0 +1,414 @@
+"""bench.py -- throughput of the B200 2DGS camera + LiDAR renderer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gsr|reference]
+                    [--workload chunked|mid|fisheye|lidar|tiny] [--streams S]
+
+One STEP = one pass of the whole hot path (gs_project -> gs_bin_sort ->
+gs_render_camera / gs_render_lidar, plus the NCCL gather to rank 0 when
+N > 1) over one batch of synthetic input.  Default workload: BASELINE.json
+configs[4], the Chunked street batch (8 x 1.5M surfels, 64 timesteps x
+{6 pinholes 1920x1080 + 1 LiDAR 64x2048} = 448 frames), frames sharded over
+the N ranks by timestep block with the surfels replicated (strong scaling:
+the batch is fixed).  Prints ONE JSON line on rank 0 (contract in DESIGN.md §8).
+
+  value     device-resident throughput, Msamples/s = (camera pixels + LiDAR
+            rays) of the batch / max-over-ranks step time (CUDA events,
+            barrier + synchronize on both sides);
+  e2e       the same through the public API with HOST buffers: per step the
+            pinned-host -> device copy of the surfels and the device -> pinned
+            host copy of every rendered frame are inside the timed region;
+  roofline  the dominant kernel (gs_render_camera, pinhole) against the FP32
+            pipe: algorithmic lane-instructions (composited pairs x 40,
+            SURVEY.md §8(d)) / its CUDA-event duration;
+  cpu_baseline  the fp64 CPU oracle (test infrastructure, oracle/) on a
+            bounded random ray sample of the same batch, on rank 0 at N = 1.
+
+`--impl reference` times that oracle alone (the reference arm of this tier:
+there is no reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rendered Mpixel/s and LiDAR Mrays/s per GPU and at 1/2/4/8 B200"
+UNIT = "Msamples/s (camera pixels + LiDAR rays)"
+# algorithmic FP32-pipe lane-instructions per composited (ray, surfel) pair
+INSTR_PER_PAIR = {0: 40, 1: 55, 2: 55}
+SM_COUNT, FP32_LANES = 148, 128
+
+
+# ------------------------------------------------------------------ workloads
+def build_workload(name, timesteps):
+    """-> (surfels (numpy), list of per-timestep sensor lists, description dict)."""
+    import scenegen as sg
+    if name == "chunked":
+        s = sg.chunked_surfels()
+        groups = [sg.chunked_timestep_sensors(t) for t in range(timesteps)]
+        desc = {"workload": f"chunked street batch: 8 chunks x 1.5M surfels (SH3), {timesteps} timesteps x "
+                            f"(6 pinhole 1920x1080 f=1200 + 1 LiDAR 64x2048) = {7 * timesteps} frames",
+                "surfels": s.n, "timesteps": timesteps, "frames": 7 * timesteps}
+    else:
+        c = sg.make_config(name)
+        s = c.surfels
+        groups = [list(c.sensors)]
+        se = c.sensors[0]
+        desc = {"workload": f"{name}: {s.n} surfels, 1 frame {se.width}x{se.height} kind {se.kind}",
+                "surfels": s.n, "timesteps": 1, "frames": len(c.sensors)}
+    return s, groups, desc
+
+
+def samples_of(sensors):
+    return sum(int(s.width) * int(s.height) for s in sensors)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="gsr_clocks_", suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, power, reasons = [], [], [], set()
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 9 or not p[0].isdigit() or int(p[0]) not in self.gpus:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    smax.append(float(p[2]))
+                    power.append(float(p[3]))
+                except ValueError:
+                    continue
+                for name, v in zip(self.NAMES, p[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
+def oracle_rate(surfels, sensors, n_rays, seed, cores, frames_per_sample=4):
+    """Time the fp64 oracle on n_rays random rays of random frames of the
+    batch.  Returns (rays/s, rays, seconds)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    fr = rng.choice(len(sensors), size=min(frames_per_sample, len(sensors)), replace=False)
+    per = max(1, n_rays // len(fr))
+    t0 = time.perf_counter()
+    done = 0
+    for f in fr:
+        se = sensors[int(f)]
+        rays = rng.choice(se.width * se.height, size=min(per, se.width * se.height), replace=False)
+        oracle.render(surfels, se, rays, nthreads=cores)
+        done += len(rays)
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def cpu_cores():
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(surfels, sensors, target_s=15.0):
+    cores = cpu_cores()
+    r0, n0, t0 = oracle_rate(surfels, sensors, 64, 1234, cores, 1)   # calibration
+    n = int(min(20000, max(64, r0 * target_s)))
+    r, n, t = oracle_rate(surfels, sensors, n, 4321, cores)
+    return {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} random rays over 4 random frames of the batch ({t:.1f} s of CPU work, "
+                      f"fp64 brute force over all {surfels.n} surfels per ray, OpenMP {cores} threads)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    surfels, groups, desc = build_workload(args.workload, args.timesteps)
+    sensors = [s for g in groups for s in g]
+    cores = cpu_cores()
+    rays_per_step = args.ref_rays
+    for w in range(args.warmup):
+        oracle_rate(surfels, sensors, rays_per_step, 10_000 + w, cores)
+    tot_rays, tot_t = 0, 0.0
+    for k in range(args.steps):
+        _, n, t = oracle_rate(surfels, sensors, rays_per_step, 20_000 + k, cores)
+        tot_rays += n
+        tot_t += t
+    value = tot_rays / tot_t / 1e6
+    desc.update(parallelism="oracle (CPU)", n_gpus_requested=args.gpus)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (scenegen, BASELINE.json configs)", "config": desc,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"each step: {rays_per_step} random rays over 4 random frames of the "
+                                       f"batch, fp64 brute force over all surfels per ray"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gsr(args):
+    import torch
+
+    from paper_2503_11731_b200 import dist as gd
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.batch import BatchRenderer, FrameTimes
+    from paper_2503_11731_b200.render import to_device
+
+    rank, world, device = gd.init()
+    if device.type != "cuda":
+        raise SystemExit("bench.py needs a CUDA device (B200)")
+    gsr.load(build_if_missing=False)   # the in-tree libgsr.so; never a fallback
+    t_gen = time.time()
+    surfels_np, groups, desc = build_workload(args.workload, args.timesteps)
+    n_steps_t = len(groups)
+    lo, hi = gd.shard_range(n_steps_t, world, rank)
+    my_sensors = [s for g in groups[lo:hi] for s in g]
+    all_sensors = [s for g in groups for s in g]
+    kinds = sorted({int(s.kind) for s in all_sensors})
+    t_gen = time.time() - t_gen
+
+    surf = to_device(surfels_np, device)
+    br = BatchRenderer(surf, device=device, n_streams=args.streams)
+    caps, contrib, evals = br.plan(my_sensors, stats=True)
+    sensors = br.wrap(my_sensors)
+
+    # output slabs per sensor kind, batch order; rank 0 holds the whole batch
+    def kind_frames(ss, k):
+        return [i for i, s in enumerate(ss) if int(s.kind) == k]
+    slabs_full, slabs_local, outs = {}, {}, [None] * len(sensors)
+    for k in kinds:
+        ref = next(s for s in all_sensors if int(s.kind) == k)
+        C = 4 if k == gsr.GS_LIDAR_SPINNING else 8
+        per_t = sum(1 for s in groups[0] if int(s.kind) == k)
+        n_all = per_t * n_steps_t
+        idx = kind_frames(my_sensors, k)
+        if rank == 0:
+            slabs_full[k] = torch.empty((n_all, C, ref.height, ref.width), dtype=torch.float32, device=device)
+            slabs_local[k] = slabs_full[k][per_t * lo: per_t * hi]
+        else:
+            slabs_local[k] = torch.empty((len(idx), C, ref.height, ref.width), dtype=torch.float32, device=device)
+        for j, i in enumerate(idx):
+            outs[i] = slabs_local[k][j]
+
+    def gather():
+        reqs = []
+        for k in kinds:
+            per_t = sum(1 for s in groups[0] if int(s.kind) == k)
+            full = slabs_full.get(k)
+            # blocks of timesteps -> blocks of frames of this kind
+            loc = slabs_local[k]
+            if world > 1:
+                fv = full.view(n_steps_t, per_t, *full.shape[1:]) if full is not None else None
+                lv = loc.view(hi - lo, per_t, *loc.shape[1:])
+                reqs += gd.gather_blocks(lv, fv, n_steps_t, world, rank)
+        for r in reqs:
+            r.wait()
+
+    def step(times=None, on_frame=None):
+        br.render(sensors, outs, times=times, on_frame=on_frame)
+        gather()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(device)
+    ovf = br.overflowed()
+    assert not ovf, f"pair capacity exceeded on frames {ovf}"
+
+    # ---------------- timed region (device-resident inputs)
+    sampler = ClockSampler(list(range(world))).start() if rank == 0 else None
+    times = FrameTimes()
+    n_launch0 = gsr.gs_kernel_launches()
+    gd.barrier(world, device)
+    torch.cuda.synchronize(device)
+    cur = torch.cuda.current_stream(device)
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(cur)
+    for _ in range(args.steps):
+        step()
+    t_all1.record(cur)
+    torch.cuda.synchronize(device)
+    gd.barrier(world, device)
+    n_launch = gsr.gs_kernel_launches() - n_launch0
+    clocks = sampler.stop() if sampler else None
+    ms_local = t_all0.elapsed_time(t_all1) / args.steps
+    ms_step = gd.max_over_ranks(ms_local, device, world)
+    total_samples = samples_of(all_sensors)
+    value = total_samples / (ms_step * 1e-3) / 1e6
+
+    # ---------------- per-kernel timing pass (events per entry point, same launch configuration)
+    for _ in range(max(1, min(args.steps, 3))):
+        br.render(sensors, outs, times=times)
+    nf = len(sensors)
+    reps = len(times.render) // nf
+    mean_by = lambda arr, idx: float(np.mean([arr[r * nf + i] for r in range(reps) for i in idx])) if idx else 0.0
+    stage = {}
+    for k in kinds:
+        idx = kind_frames(my_sensors, k)
+        stage[{0: "pinhole", 1: "fisheye", 2: "lidar"}[k]] = {
+            "frames": len(idx), "ms_project": round(mean_by(times.project, idx), 4),
+            "ms_bin_sort": round(mean_by(times.sort, idx), 4), "ms_render": round(mean_by(times.render, idx), 4),
+            "pairs_mean": int(np.mean([caps[i] for i in idx])),
+            "composited_per_sample": round(float(np.sum([contrib[i] for i in idx])) /
+                                           max(1, samples_of([my_sensors[i] for i in idx])), 2),
+            "evaluated_per_sample": round(float(np.sum([evals[i] for i in idx])) /
+                                          max(1, samples_of([my_sensors[i] for i in idx])), 2)}
+    # dominant kernel: the compositing call of the most frequent camera kind
+    dom_kind = 0 if 0 in kinds else kinds[0]
+    idx = kind_frames(my_sensors, dom_kind)
+    t_render = mean_by(times.render, idx) * 1e-3
+    instr = float(np.mean([contrib[i] for i in idx])) * INSTR_PER_PAIR[dom_kind]
+    clk = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = SM_COUNT * FP32_LANES * clk * 1e6 / 1e12
+    achieved = instr / t_render / 1e12 if t_render > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{args.workload}:{dom_kind}")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"kernel": f"gs_render_camera ({'pinhole' if dom_kind == 0 else 'kind %d' % dom_kind})",
+                "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 2), "unit": "Tinst/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "work": f"{INSTR_PER_PAIR[dom_kind]} FP32 lane-instr x composited pairs per launch "
+                        f"(mean {int(np.mean([contrib[i] for i in idx]))}), peak = {SM_COUNT} SMs x {FP32_LANES} "
+                        f"FP32 lanes x {clk:.0f} MHz (sm_max)",
+                "ms_per_launch": round(t_render * 1e3, 4)}
+
+    # ---------------- end to end: host buffers through the public API
+    e2e = None
+    if not args.no_e2e:
+        host = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in surf.items()}
+        h2d = sum(v.numel() * v.element_size() for v in host.values() if isinstance(v, torch.Tensor))
+        host_out = {k: torch.empty(slabs_local[k].shape, dtype=torch.float32, pin_memory=True) for k in kinds}
+        host_views = [None] * len(sensors)
+        for k in kinds:
+            for j, i in enumerate(kind_frames(my_sensors, k)):
+                host_views[i] = host_out[k][j]
+        d2h = sum(t.numel() * 4 for t in host_out.values())
+        copy_stream = torch.cuda.Stream(device)
+
+        def on_frame(i, st):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            copy_stream.wait_event(ev)
+            with torch.cuda.stream(copy_stream):
+                host_views[i].copy_(outs[i], non_blocking=True)
+
+        def e2e_step():
+            for k, v in host.items():
+                if isinstance(v, torch.Tensor):
+                    surf[k].copy_(v, non_blocking=True)
+            br.render(sensors, outs, on_frame=on_frame)
+            cur.wait_stream(copy_stream)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        gd.barrier(world, device)
+        torch.cuda.synchronize(device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(cur)
+        torch.cuda.synchronize(device)
+        gd.barrier(world, device)
+        ms_e2e = gd.max_over_ranks(a.elapsed_time(b) / args.steps, device, world)
+        assert not br.overflowed()
+        e2e = {"value": total_samples / (ms_e2e * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms_e2e, 3),
+               "path": "pinned host surfels -> device, BatchRenderer (C-ABI), every frame -> pinned host on a "
+                       "copy stream overlapping the next frames; per rank, no gather"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(surfels_np, all_sensors, args.cpu_seconds)
+
+    if rank == 0:
+        desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
+                    if world > 1 else "1 GPU", streams=args.streams,
+                    l2="no flush: resident surfels (%.2f GB) and outputs (%.1f GB) exceed the 126 MB L2" % (
+                        sum(v.numel() * 4 for v in surf.values() if isinstance(v, torch.Tensor)) / 1e9,
+                        sum(t.numel() * 4 for t in slabs_full.values()) / 1e9))
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenegen seeds, "
+                "BASELINE.json configs; random surfels, no trained scene)", "config": desc,
+                "e2e": e2e, "gpu_launches": int(n_launch), "gpu_launches_per_step": n_launch // args.steps,
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "stages": stage,
+                "setup_s": {"generate": round(t_gen, 1)}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
+    ap.add_argument("--workload", default="chunked", choices=["chunked", "mid", "fisheye", "lidar", "tiny"])
+    ap.add_argument("--timesteps", type=int, default=64)
+    ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-rays", type=int, default=256)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gsr(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -201,6 +201,11 @@ gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *valu
 const char *gs_status_string(gs_status status);
 const char *gs_last_error(void);
 
+/* Cumulative number of CUDA kernels this library has launched in the process
+ * (all entry points, all streams; memsets are not counted).  Diagnostic: the
+ * difference across a region counts the library's launches in it. */
+uint64_t gs_kernel_launches(void);
+
 /* Bytes of one projected surfel record for this sensor kind (debug/tests). */
 int32_t gs_record_bytes(int32_t kind);
 

@@ -1,0 +1,107 @@
+"""Batched multi-frame rendering through the C-ABI (many sensor frames over
+one resident surfel set), e.g. the Chunked street batch of BASELINE.json
+(timesteps x {6 pinholes + 1 LiDAR}).
+
+`BatchRenderer` owns `n_streams` lanes (a `Renderer` buffer set + a CUDA
+stream each) and deals frames to them round-robin, so the short serial
+kernels of one frame (scans, look-back passes, schedule) overlap the long
+ones of the next.  It runs in capacity mode: `plan()` sizes every frame's
+pair buffers once (one sync per frame, outside any timed region) and
+`render()` is then free of host synchronisation.  Every frame gets its own
+overflow slot; `overflowed()` lists frames whose capacity was exceeded.
+
+This module marshals buffers only; all arithmetic runs in libgsr.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import gsr
+from .render import Renderer, n_channels
+
+
+@dataclass
+class FrameTimes:
+    """Per-frame CUDA-event durations (ms) of the three entry points."""
+    project: list = field(default_factory=list)
+    sort: list = field(default_factory=list)
+    render: list = field(default_factory=list)
+
+
+class BatchRenderer:
+    def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
+                 lidar_tile=(32, 1)):
+        self.device = torch.device(device)
+        self.lanes = [Renderer(surfels, opts, device, lidar_tile) for _ in range(max(1, n_streams))]
+        self.streams = [torch.cuda.Stream(self.device) for _ in self.lanes]
+        self.n = self.lanes[0].n
+        self.caps = None
+        self.ovf = None
+
+    @staticmethod
+    def wrap(sensors):
+        return [s if isinstance(s, gsr.Sensor) else gsr.Sensor(s) for s in sensors]
+
+    def alloc_outputs(self, sensors):
+        """One planar fp32 output tensor per frame ([8,H,W] camera, [4,H,W] LiDAR)."""
+        return [torch.empty((n_channels(s.kind), s.height, s.width), dtype=torch.float32,
+                            device=self.device) for s in sensors]
+
+    def plan(self, sensors, stats: bool = False):
+        """Exact pair count of every frame -> its capacity (one sync per
+        frame).  With stats=True also returns, per frame, the number of
+        composited (ray, surfel) pairs and of pairs whose conservative pixel
+        box contains the ray (instrumented unsplit kernel)."""
+        sensors = self.wrap(sensors)
+        lane = self.lanes[0]
+        caps, contrib, evals = [], [], []
+        for s in sensors:
+            _, d_np = lane.project(s)
+            caps.append(int(d_np.item()))
+        self.caps = caps
+        self.ovf = torch.zeros(len(sensors), dtype=torch.int32, device=self.device)
+        if stats:
+            for s, cap in zip(sensors, caps):
+                st = torch.zeros((2, s.height, s.width), dtype=torch.int32, device=self.device)
+                lane.render(s, capacity=cap, stats=st)
+                tot = st.view(2, -1).sum(dim=1, dtype=torch.int64).cpu()
+                contrib.append(int(tot[0]))
+                evals.append(int(tot[1]))
+        torch.cuda.synchronize(self.device)
+        return (caps, contrib, evals) if stats else caps
+
+    def render(self, sensors, outs, times: FrameTimes | None = None, on_frame=None):
+        """Render frame i into outs[i] on lane i % n_streams.  times: if given,
+        per-frame event durations are appended after the batch completes
+        (this synchronises).  on_frame(i, stream): called right after frame i
+        is enqueued (e.g. to chain a device->host copy)."""
+        sensors = self.wrap(sensors)
+        assert self.caps is not None and len(self.caps) == len(sensors), "call plan() first"
+        cur = torch.cuda.current_stream(self.device)
+        for st in self.streams:
+            st.wait_stream(cur)
+        evs = []
+        for i, s in enumerate(sensors):
+            k = i % len(self.lanes)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if times is not None else None
+            with torch.cuda.stream(self.streams[k]):
+                self.lanes[k].render(s, out=outs[i], capacity=self.caps[i], events=ev,
+                                     overflow=self.ovf[i:i + 1])
+                if on_frame is not None:
+                    on_frame(i, self.streams[k])
+            evs.append(ev)
+        for st in self.streams:
+            cur.wait_stream(st)
+        if times is not None:
+            torch.cuda.synchronize(self.device)
+            for ev in evs:
+                times.project.append(ev[0].elapsed_time(ev[1]))
+                times.sort.append(ev[1].elapsed_time(ev[2]))
+                times.render.append(ev[2].elapsed_time(ev[3]))
+        return outs
+
+    def overflowed(self):
+        """Indices of frames of the last render() whose pair capacity was exceeded."""
+        return torch.nonzero(self.ovf).flatten().tolist()

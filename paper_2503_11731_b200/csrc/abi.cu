@@ -5,6 +5,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "gsr_internal.cuh"
 
 namespace gsr {
@@ -26,6 +28,13 @@ cudaError_t launch_render_lidar(const void *, int64_t, const uint32_t *, const u
 using namespace gsr;
 
 static thread_local char g_err[512];
+static std::atomic<unsigned long long> g_launches{0};
+
+namespace gsr {
+void note_launch(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+}  // namespace gsr
+
+extern "C" uint64_t gs_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 static gs_status fail(gs_status s, const char *fmt, const char *arg = "") {
     snprintf(g_err, sizeof(g_err), fmt, arg);

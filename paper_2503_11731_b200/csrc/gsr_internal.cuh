@@ -114,6 +114,10 @@ struct ProjLayout {
 };
 
 // ---------------------------------------------------------------- helpers
+// Process-wide count of kernels launched by the library (diagnostic for
+// gs_kernel_launches(); the only mutable state, a relaxed atomic).
+void note_launch(int k = 1);
+
 __device__ __forceinline__ void split_hilo(double x, float &hi, float &lo) {
     hi = (float)x;
     lo = (float)(x - (double)hi);

@@ -636,6 +636,7 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
         k_project<GS_FISHEYE_EQUIDISTANT><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
     else
         k_project<GS_LIDAR_SPINNING><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
+    note_launch(2);   // k_project + k_compact
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     unsigned long long *stv = (unsigned long long *)(base + L.status);

@@ -525,6 +525,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
     if (e != cudaSuccess) return e;
     const unsigned gt = (unsigned)((ntiles + 255) / 256);
+    note_launch(3);
     k_sched_count<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, L);
     k_sched_scan<<<1, 32, 0, st>>>(h);
     k_sched_fill<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, items, split_base, split_list, L);
@@ -539,6 +540,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, WARPS * 32, sm);
     const unsigned grid = (unsigned)std::max(1, std::min(nsm * std::max(per, 1), (ntiles + WARPS - 1) / WARPS + nsm));
+    note_launch();
     k_render<KIND, STATS><<<grid, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
                                                         items, split_base, partials, o0, o1, o2, o3, stats, L);
     e = cudaGetLastError();
@@ -546,6 +548,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     if (!STATS && W.max_split > 0) {
         e = cudaFuncSetAttribute(k_merge<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
+        note_launch();
         k_merge<KIND><<<W.max_split, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_base,
                                                            split_list, partials, o0, o1, o2, o3, L);
         e = cudaGetLastError();

@@ -360,6 +360,7 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     const uint32_t *d_nvis = &hdr->n_visible;
     // 1. depth sort of the visible surfels (4 x 8-bit digits)
     const unsigned hgrid_d = (unsigned)std::min<int64_t>((n + 4095) / 4096, 4 * 148);
+    note_launch();
     k_hist<<<hgrid_d > 0 ? hgrid_d : 1, 256, 0, st>>>((const uint32_t *)(pb + L.vkey), d_nvis, 4, 32,
                                                       hist, nullptr);
     CK(cudaGetLastError());
@@ -367,10 +368,12 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     uint32_t *bufk[2] = {(uint32_t *)(wb + W.dA_k), (uint32_t *)(wb + W.dB_k)};
     uint32_t *bufv[2] = {(uint32_t *)(wb + W.dA_v), (uint32_t *)(wb + W.dB_v)};
     // the depth histogram scan and the tile histogram share `hist` rows 0..3 / 4..6
+    note_launch();
     k_hist_scan<<<1, RS_BINS, 0, st>>>(hist, 4, nullptr);
     CK(cudaGetLastError());
     const unsigned grid_d = (unsigned)(W.ntile_d > 0 ? W.ntile_d : 1);
     for (int p = 0; p < 4; ++p) {
+        note_launch();
         k_onesweep<<<grid_d, RS_THREADS, 0, st>>>(ki, vi, bufk[p & 1], bufv[p & 1], d_nvis, 8 * p, 8,
                                                   hist + p * RS_BINS,
                                                   (uint32_t *)(wb + W.dstat) + (size_t)p * W.ntile_d * RS_BINS,
@@ -383,6 +386,7 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     const uint32_t *sid = vi;
     uint32_t *offs = (uint32_t *)(wb + W.offs);
     const unsigned gridc = (unsigned)(W.nblk_c > 0 ? W.nblk_c : 1);
+    note_launch();
     k_pair_offsets<<<gridc, SCAN_THREADS, 0, st>>>(sid, (const uint32_t *)(pb + L.cnt), hdr, offs,
                                                    (unsigned long long *)(wb + W.cstat), misc, cap,
                                                    d_overflow);
@@ -392,6 +396,7 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     uint32_t *tk[2] = {(uint32_t *)(wb + W.tk0), (uint32_t *)(wb + W.tk1)};
     uint32_t *tv[2] = {values, (uint32_t *)(wb + W.tv1)};
     int cur = np & 1;
+    note_launch();
     k_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr,
                                                          ntx, tk[cur], tv[cur], d_overflow);
     CK(cudaGetLastError());
@@ -400,13 +405,16 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     const uint32_t *d_np = &misc->n_pairs32;
     uint32_t *thist = hist + 4 * RS_BINS;
     const unsigned hgrid_t = (unsigned)std::min<int64_t>((cap + 4095) / 4096, 4 * 148);
+    note_launch();
     k_hist<<<hgrid_t > 0 ? hgrid_t : 1, 256, 0, st>>>(tk[cur], d_np, np, tb, thist, d_overflow);
     CK(cudaGetLastError());
+    note_launch();
     k_hist_scan<<<1, RS_BINS, 0, st>>>(thist, np, d_overflow);
     CK(cudaGetLastError());
     const unsigned grid_t = (unsigned)(W.ntile_t > 0 ? W.ntile_t : 1);
     for (int p = 0; p < np; ++p) {
         const int bits = min(8, tb - 8 * p);
+        note_launch();
         k_onesweep<<<grid_t, RS_THREADS, 0, st>>>(tk[cur], tv[cur], tk[cur ^ 1], tv[cur ^ 1], d_np, 8 * p,
                                                   bits, thist + p * RS_BINS,
                                                   (uint32_t *)(wb + W.tstat) + (size_t)p * W.ntile_t * RS_BINS,
@@ -416,9 +424,11 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     }
     // cur == 0 now: sorted tile keys in tk[0], values in `values`
     const unsigned gp = (unsigned)((cap + 255) / 256);
+    note_launch();
     k_ranges<<<gp > 0 ? gp : 1, 256, 0, st>>>(tk[cur], misc, ranges, d_overflow);
     CK(cudaGetLastError());
     if (keys) {
+        note_launch();
         k_keys64<<<gp > 0 ? gp : 1, 256, 0, st>>>(tk[cur], values, (const uint32_t *)(pb + L.key), misc,
                                                   (unsigned long long *)keys, d_overflow);
         CK(cudaGetLastError());

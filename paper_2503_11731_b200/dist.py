@@ -1,0 +1,104 @@
+"""Frame-sharded multi-GPU rendering (BASELINE.json north_star).
+
+The surfel set is replicated on every rank; sensor frames are sharded by
+TIMESTEP in contiguous blocks (rank r renders timesteps [lo_r, hi_r), all
+sensors of each), so each rank's frames are one contiguous slice of the
+batch-ordered output and the only exchange step -- the final gather of the
+frames to rank 0 -- lands every peer's slice directly in rank 0's output
+slab with one point-to-point receive (NCCL over NVLink on GPUs, gloo in the
+CPU tests).  No collective touches the data path before the gather, and
+frames are never split across ranks (depth-ordered compositing does not
+shard).  Contiguous blocks keep the camera/LiDAR mix identical per rank;
+the street generator is uniform along the road, so per-timestep cost is
+flat and blocks balance as well as a round-robin deal would.
+"""
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def env_world():
+    """(rank, world_size, local_rank) from the torchrun environment (1 process if unset)."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init(backend: str | None = None):
+    """Initialise the default process group when WORLD_SIZE > 1.
+    Returns (rank, world, device)."""
+    rank, world, local = env_world()
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+        device = torch.device("cuda", local)
+    else:
+        device = torch.device("cpu")
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        be = backend or ("nccl" if device.type == "cuda" else "gloo")
+        kw = dict(backend=be, rank=rank, world_size=world)
+        if be == "nccl":
+            kw["device_id"] = device
+        dist.init_process_group(**kw)
+    return rank, world, device
+
+
+def shard_range(n_items: int, world: int, rank: int):
+    """Contiguous block [lo, hi) of n_items for `rank`; the first
+    n_items % world ranks get one extra item."""
+    base, extra = divmod(n_items, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def shard_counts(n_items: int, world: int):
+    return [shard_range(n_items, world, r)[1] - shard_range(n_items, world, r)[0] for r in range(world)]
+
+
+def gather_blocks(local: torch.Tensor, full: torch.Tensor | None, n_items: int, world: int, rank: int,
+                  root: int = 0, group=None):
+    """Gather every rank's contiguous block of a batch (dim 0) into `full`
+    on `root` with point-to-point transfers (one recv per peer into the
+    peer's slice of `full`; the root's own block is copied unless `local`
+    already is that slice).  `local` has shard_counts(...)[rank] rows.
+    Returns the list of outstanding requests (wait() them, or let the
+    caller's stream order them on NCCL)."""
+    if world == 1:
+        if full is not None and local.data_ptr() != full.data_ptr():
+            full.copy_(local)
+        return []
+    ops = []
+    if rank == root:
+        assert full is not None and full.shape[0] == n_items
+        for r in range(world):
+            lo, hi = shard_range(n_items, world, r)
+            if r == root:
+                if local.data_ptr() != full[lo:hi].data_ptr() and hi > lo:
+                    full[lo:hi].copy_(local)
+            elif hi > lo:
+                ops.append(dist.P2POp(dist.irecv, full[lo:hi], r, group))
+    else:
+        if local.shape[0] > 0:
+            ops.append(dist.P2POp(dist.isend, local.contiguous(), root, group))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+def max_over_ranks(x: float, device, world: int) -> float:
+    """Device-timed quantity -> its maximum over ranks."""
+    if world == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int, device=None):
+    if world > 1:
+        if device is not None and device.type == "cuda":
+            dist.barrier(device_ids=[device.index])
+        else:
+            dist.barrier()

@@ -52,7 +52,8 @@ class gs_opts(C.Structure):
 
 EXPORTS = ["gs_default_opts", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
-           "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes"]
+           "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes",
+           "gs_kernel_launches"]
 
 _lib = None
 
@@ -98,6 +99,8 @@ def load(build_if_missing: bool = True):
     lib.gs_status_string.restype = C.c_char_p
     lib.gs_last_error.argtypes = []
     lib.gs_last_error.restype = C.c_char_p
+    lib.gs_kernel_launches.argtypes = []
+    lib.gs_kernel_launches.restype = C.c_uint64
     _lib = lib
     return lib
 
@@ -219,3 +222,7 @@ def gs_render_lidar(projected, n, values, tile_ranges, d_overflow, sensor: Senso
                                   workspace.numel() * workspace.element_size(), _ptr(rng),
                                   _ptr(intensity), _ptr(raydrop), _ptr(alpha), _ptr(stats),
                                   C.c_void_p(stream)))
+
+
+def gs_kernel_launches() -> int:
+    return int(load().gs_kernel_launches())

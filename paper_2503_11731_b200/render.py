@@ -71,12 +71,14 @@ class Renderer:
 
     def render(self, sensor, out: torch.Tensor | None = None, capacity: int | None = None,
                keys: bool = False, stream=None, stats: torch.Tensor | None = None,
-               events=None) -> torch.Tensor:
+               events=None, overflow: torch.Tensor | None = None) -> torch.Tensor:
         """Render one frame; returns a planar fp32 tensor [C,H,W] (C = 8 for
         cameras: r,g,b,depth,nx,ny,nz,alpha; 4 for LiDAR: range, intensity,
         raydrop, alpha).  stats: optional int32 [2,H,W] (composited, evaluated
         pairs per sample).  events: optional 4 CUDA events recorded before
-        gs_project, gs_bin_sort, the render call and after it."""
+        gs_project, gs_bin_sort, the render call and after it.  overflow:
+        optional int32 device slot for gs_bin_sort's overflow flag (default:
+        a buffer owned by the renderer)."""
         if not isinstance(sensor, gsr.Sensor):
             sensor = gsr.Sensor(sensor)
         self.opts = self.lidar_opts if sensor.kind == gsr.GS_LIDAR_SPINNING else self.cam_opts
@@ -95,7 +97,7 @@ class Renderer:
         nt = gsr.gs_num_tiles(sensor, self.opts)
         values = self._i32("values", cap)
         ranges = self._i32("ranges", 2 * nt)
-        ovf = self._i32("overflow", 1)
+        ovf = overflow if overflow is not None else self._i32("overflow", 1)
         ws = self._get("ws", gsr.gs_sort_workspace_bytes(self.n, cap, sensor, self.opts))
         kbuf = self._get("keys", 8 * max(cap, 1))[: 8 * max(cap, 1)].view(torch.int64) if keys else None
         gsr.gs_bin_sort(proj, self.n, sensor, self.opts, kbuf, values, cap, ranges, ws, ovf, st)

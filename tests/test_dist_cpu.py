@@ -1,0 +1,89 @@
+"""Host logic of the frame-sharded multi-GPU path (paper_2503_11731_b200/dist.py)
+on CPU: shard plans, and the gather of per-rank frame blocks to rank 0 over a
+world_size-2 (and 3) gloo process group."""
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_2503_11731_b200 import dist as gd  # noqa: E402
+
+
+@pytest.mark.parametrize("n,world", [(64, 1), (64, 2), (64, 8), (7, 3), (3, 4), (0, 2)])
+def test_shard_range_partitions(n, world):
+    seen = []
+    for r in range(world):
+        lo, hi = gd.shard_range(n, world, r)
+        assert 0 <= lo <= hi <= n
+        seen += list(range(lo, hi))
+    assert seen == list(range(n))            # contiguous, ordered, disjoint, complete
+    c = gd.shard_counts(n, world)
+    assert max(c) - min(c) <= 1 and sum(c) == n
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _frame(t, shape):
+    """Deterministic stand-in for the rendered frames of timestep t."""
+    g = torch.Generator().manual_seed(1000 + t)
+    return torch.rand(shape, generator=g)
+
+
+def _worker(rank, world, port, n_t, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        per_t, shape = 3, (2, 5, 4)
+        lo, hi = gd.shard_range(n_t, world, rank)
+        full = torch.full((n_t, per_t) + shape, -1.0) if rank == 0 else None
+        if rank == 0:   # the root renders straight into its slice of the batch
+            local = full[lo:hi]
+        else:
+            local = torch.empty((hi - lo, per_t) + shape)
+        for j, t in enumerate(range(lo, hi)):
+            local[j] = _frame(t, (per_t,) + shape)
+        for r in gd.gather_blocks(local, full, n_t, world, rank):
+            r.wait()
+        m = gd.max_over_ranks(float(rank) + 0.5, torch.device("cpu"), world)
+        if rank == 0:
+            want = torch.stack([_frame(t, (per_t,) + shape) for t in range(n_t)])
+            q.put(("ok", bool(torch.equal(full, want)), m))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced through the queue
+        q.put(("err", repr(e), None))
+
+
+@pytest.mark.parametrize("world,n_t", [(2, 8), (2, 5), (3, 7)])
+def test_gather_blocks_gloo(world, n_t):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n_t, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == "ok", res
+    assert res[1], "gathered batch differs from the frames the ranks rendered"
+    assert res[2] == world - 0.5                 # max over ranks
+    assert all(p.exitcode == 0 for p in ps)
+
+
+def test_gather_world1_copies():
+    local = torch.arange(12.0).view(3, 4)
+    full = torch.zeros(3, 4)
+    assert gd.gather_blocks(local, full, 3, 1, 0) == []
+    assert torch.equal(full, local)
