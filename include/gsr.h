@@ -17,8 +17,9 @@
  *     launch: GS_ERR_CONFIG (null required pointer, wrong sensor kind for the
  *     call, sh_degree outside 0..3, width/height < 1, buffer too small),
  *     GS_ERR_RANGE (focal <= 0, non-monotone beam table, azimuth span outside
- *     (0, 2pi], theta_max outside (0, pi), tile shape outside 1..512
- *     threads), GS_ERR_CUDA (launch failure, from cudaGetLastError).  On any
+ *     (0, 2pi], theta_max outside (0, pi), tile shape outside 32..512
+ *     samples or not a multiple of a 32-sample warp sub-tile), GS_ERR_CUDA
+ *     (launch failure, from cudaGetLastError).  On any
  *     error nothing is enqueued after the failing launch; gs_last_error()
  *     returns a thread-local message.  Non-finite surfel inputs are not an
  *     error: such surfels are culled.
@@ -93,10 +94,13 @@ typedef struct {
 
 /* Compositing constants (north_star); gs_default_opts() fills the defaults. */
 typedef struct {
-    int32_t tile_w, tile_h;      /* 8 x 4: one tile = the samples of one warp;
-                                    tile_w*tile_h in 1..32 (LiDAR: 32 x 1 recommended) */
+    int32_t tile_w, tile_h;      /* binning tile = the samples one CTA composites (16 x 8):
+                                    32..512 samples, a multiple of a 32-sample warp
+                                    sub-tile (cameras 8x4, then 16x2, 32x1; LiDAR 32x1,
+                                    then 16x2, 8x4); GS_ERR_RANGE otherwise.  LiDAR:
+                                    32 x 1 recommended.  Edge tiles may be partial.     */
     int32_t split_len;           /* tile lists longer than this are split into segments
-                                    composited in parallel and merged (0 = 2048;
+                                    composited in parallel and merged (0 = 16384;
                                     INT32_MAX disables splitting)                        */
     float near_plane;            /* 0.2 m                                               */
     float alpha_max;             /* 0.99                                                */

@@ -16,7 +16,7 @@ size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles);
 cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
                             int32_t *d_overflow, cudaStream_t st);
-size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len);
+size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix);
 cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
                                  const int32_t *, const DevSensor &, const DevOpts &, int32_t, void *,
                                  size_t, float *, float *, float *, float *, uint32_t *, cudaStream_t);
@@ -47,8 +47,8 @@ static gs_status cuda_fail(cudaError_t e, const char *where) {
 
 extern "C" void gs_default_opts(gs_opts *o) {
     if (!o) return;
-    o->tile_w = 8;
-    o->tile_h = 4;
+    o->tile_w = 16;
+    o->tile_h = 8;
     o->split_len = 0;
     o->near_plane = 0.2f;
     o->alpha_max = 0.99f;
@@ -76,8 +76,8 @@ extern "C" void gs_projected_offsets(int64_t n, int32_t kind, size_t offs[5]) {
 
 static gs_status check_opts(const gs_opts *o) {
     if (!o) return fail(GS_ERR_CONFIG, "opts is NULL");
-    if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 32)
-        return fail(GS_ERR_RANGE, "tile shape must hold 1..32 samples (one warp)");
+    if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 512)
+        return fail(GS_ERR_RANGE, "tile shape must hold 32..512 samples");
     if (o->split_len < 0) return fail(GS_ERR_RANGE, "split_len must be >= 0");
     if (!(o->near_plane > 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max <= 1.f) ||
         !(o->alpha_min >= 0.f) || !(o->t_min >= 0.f) || !(o->support_rho > 0.f) ||
@@ -108,6 +108,26 @@ static gs_status check_sensor(const gs_sensor *s) {
     return GS_OK;
 }
 
+// Warp sub-tile of a binning tile: 32 samples, 8x4 / 16x2 / 32x1, the first
+// that divides the tile in the kind's order of preference (LiDAR rows are
+// beams: prefer one beam per warp).  Returns false if none divides it.
+static bool warp_subtile(int32_t kind, int32_t tw, int32_t th, int32_t *sw, int32_t *sh) {
+    static const int32_t cam[3] = {8, 16, 32}, lid[3] = {32, 16, 8};
+    const int32_t *pref = kind == GS_LIDAR_SPINNING ? lid : cam;
+    for (int i = 0; i < 3; ++i) {
+        const int32_t w = pref[i], h = 32 / pref[i];
+        if (tw % w == 0 && th % h == 0) { *sw = w; *sh = h; return true; }
+    }
+    return false;
+}
+
+static gs_status check_tiles(const gs_sensor *s, const gs_opts *o) {
+    int32_t sw, sh;
+    if (!warp_subtile(s->kind, o->tile_w, o->tile_h, &sw, &sh))
+        return fail(GS_ERR_RANGE, "tile shape must be a multiple of a 32-sample warp sub-tile (8x4, 16x2, 32x1)");
+    return GS_OK;
+}
+
 static DevSensor make_dev_sensor(const gs_sensor *s, const gs_opts *o) {
     DevSensor d;
     memset(&d, 0, sizeof(d));
@@ -118,6 +138,7 @@ static DevSensor make_dev_sensor(const gs_sensor *s, const gs_opts *o) {
     d.th = o->tile_h;
     d.ntx = (s->width + o->tile_w - 1) / o->tile_w;
     d.nty = (s->height + o->tile_h - 1) / o->tile_h;
+    warp_subtile(s->kind, o->tile_w, o->tile_h, &d.sw, &d.sh);
     for (int r = 0; r < 3; ++r) {
         for (int c = 0; c < 3; ++c) d.R[3 * r + c] = s->world_to_sensor[4 * r + c];
         d.t[r] = s->world_to_sensor[4 * r + 3];
@@ -161,7 +182,7 @@ static DevOpts make_dev_opts(const gs_opts *o) {
 }
 
 extern "C" int64_t gs_num_tiles(const gs_sensor *s, const gs_opts *o) {
-    if (check_sensor(s) != GS_OK || check_opts(o) != GS_OK) return -1;
+    if (check_sensor(s) != GS_OK || check_opts(o) != GS_OK || check_tiles(s, o) != GS_OK) return -1;
     return (int64_t)((s->width + o->tile_w - 1) / o->tile_w) * ((s->height + o->tile_h - 1) / o->tile_h);
 }
 
@@ -176,6 +197,7 @@ extern "C" gs_status gs_project(const gs_surfels *sf, const gs_sensor *s, const 
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
+    if ((st = check_tiles(s, o)) != GS_OK) return st;
     if (!sf) return fail(GS_ERR_CONFIG, "surfels is NULL");
     if (sf->n < 0 || sf->n >= (1ll << 30)) return fail(GS_ERR_RANGE, "surfel count outside [0, 2^30)");
     if (!projected) return fail(GS_ERR_CONFIG, "projected is NULL");
@@ -189,6 +211,8 @@ extern "C" gs_status gs_project(const gs_surfels *sf, const gs_sensor *s, const 
             if (sf->sh_degree < 0 || sf->sh_degree > 3) return fail(GS_ERR_CONFIG, "sh_degree outside 0..3");
         }
         if (((uintptr_t)sf->quats & 15) != 0) return fail(GS_ERR_CONFIG, "quats must be 16-byte aligned");
+        if (((uintptr_t)sf->scales & 7) != 0) return fail(GS_ERR_CONFIG, "scales must be 8-byte aligned");
+        if (sf->sh && ((uintptr_t)sf->sh & 15) != 0) return fail(GS_ERR_CONFIG, "sh must be 16-byte aligned");
     }
     if (((uintptr_t)projected & 255) != 0) return fail(GS_ERR_CONFIG, "projected must be 256-byte aligned");
     DevSurfels ds;
@@ -210,6 +234,7 @@ extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sens
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
+    if ((st = check_tiles(s, o)) != GS_OK) return st;
     if (n < 0 || n >= (1ll << 30)) return fail(GS_ERR_RANGE, "surfel count outside [0, 2^30)");
     if (cap < 0 || cap >= (1ll << 30)) return fail(GS_ERR_RANGE, "pair capacity outside [0, 2^30)");
     if (!projected || !tile_ranges || !d_overflow || !workspace || (cap > 0 && !values))
@@ -227,13 +252,13 @@ extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sens
 extern "C" size_t gs_render_workspace_bytes(int64_t cap, const gs_sensor *s, const gs_opts *o) {
     const int64_t nt = gs_num_tiles(s, o);
     if (nt < 0 || cap < 0) return 0;
-    return render_workspace_bytes(cap, nt, o->split_len);
+    return render_workspace_bytes(cap, nt, o->split_len, o->tile_w * o->tile_h);
 }
 
 static gs_status check_render(const void *projected, const uint32_t *tile_ranges, const float *alpha,
                               const gs_sensor *s, const gs_opts *o, void *ws, size_t ws_bytes) {
     if (!projected || !tile_ranges || !alpha || !ws) return fail(GS_ERR_CONFIG, "null buffer");
-    if (ws_bytes < render_workspace_bytes(0, gs_num_tiles(s, o), o->split_len))
+    if (ws_bytes < render_workspace_bytes(0, gs_num_tiles(s, o), o->split_len, o->tile_w * o->tile_h))
         return fail(GS_ERR_CONFIG, "render workspace too small");
     return GS_OK;
 }
@@ -246,6 +271,7 @@ extern "C" gs_status gs_render_camera(const void *projected, int64_t n, const ui
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
+    if ((st = check_tiles(s, o)) != GS_OK) return st;
     if (s->kind == GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_camera called with a LiDAR sensor");
     if ((st = check_render(projected, tile_ranges, alpha, s, o, workspace, workspace_bytes)) != GS_OK) return st;
     const DevSensor se = make_dev_sensor(s, o);
@@ -265,6 +291,7 @@ extern "C" gs_status gs_render_lidar(const void *projected, int64_t n, const uin
     gs_status st;
     if ((st = check_sensor(s)) != GS_OK) return st;
     if ((st = check_opts(o)) != GS_OK) return st;
+    if ((st = check_tiles(s, o)) != GS_OK) return st;
     if (s->kind != GS_LIDAR_SPINNING) return fail(GS_ERR_CONFIG, "gs_render_lidar called with a camera sensor");
     if ((st = check_render(projected, tile_ranges, alpha, s, o, workspace, workspace_bytes)) != GS_OK) return st;
     const DevSensor se = make_dev_sensor(s, o);

@@ -12,7 +12,8 @@ namespace gsr {
 // ---------------------------------------------------------------- params
 struct DevSensor {
     int32_t kind, width, height;
-    int32_t tw, th, ntx, nty;
+    int32_t tw, th, ntx, nty;   // binning tile (one CTA) and tile grid
+    int32_t sw, sh;             // warp sub-tile (32 samples: 8x4, 16x2 or 32x1)
     float R[9], t[3];           // world -> sensor
     float fx, fy, cx, cy;
     float k[4];
@@ -81,35 +82,37 @@ __host__ __device__ inline int record_floats(int kind) {
 
 // ---------------------------------------------------------------- projected buffer
 // [ header 256 B | records n*rec | rect n*8 | key n*4 | count n*4 |
-//   vis_key n*4 | vis_id n*4 | scan status 2*nblk*8 ]
+//   vis_key n*4 | vis_id n*4 | cand n*4 | scan status 3*(nblk+1)*8 ]
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
 
 struct ProjHeader {
     uint32_t n_visible;
-    uint32_t pad0;
+    uint32_t n_cand;            // surfels that pass the conservative cull (k_cull)
     int64_t num_pairs;
     uint32_t scan_counter;      // dynamic tile id for the compaction scan
-    uint32_t pad1[59];
+    uint32_t cull_counter;      // dynamic tile id for the cull scan
+    uint32_t pad1[58];
 };
 static_assert(sizeof(ProjHeader) == 256, "header");
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjLayout {
-    size_t rec, rect, key, cnt, vkey, vid, status, total;
+    size_t rec, rect, key, cnt, vkey, vid, cand, status, nblk, total;
     __host__ __device__ ProjLayout(int64_t n, int kind) {
         size_t N = (size_t)(n > 0 ? n : 0);
-        size_t nblk = (N + SCAN_TILE - 1) / SCAN_TILE;
+        nblk = (N + SCAN_TILE - 1) / SCAN_TILE;
         rec = 256;
         rect = rec + align256(N * record_floats(kind) * 4);
         key = rect + align256(N * 8);
         cnt = key + align256(N * 4);
         vkey = cnt + align256(N * 4);
         vid = vkey + align256(N * 4);
-        status = vid + align256(N * 4);
-        total = status + align256(2 * (nblk + 1) * 8);
+        cand = vid + align256(N * 4);
+        status = cand + align256(N * 4);
+        total = status + align256(3 * (nblk + 1) * 8);
     }
 };
 

@@ -9,6 +9,8 @@
 // sees well-conditioned, centre-relative values.
 #include <math.h>
 
+#include <algorithm>
+
 #include "gsr_internal.cuh"
 #include "scan.cuh"
 
@@ -138,10 +140,26 @@ __device__ __forceinline__ void sh_colour(const float *sh, int deg, float x, flo
         }
     }
     float r = 0.f, g = 0.f, bl = 0.f;
-    for (int j = 0; j < nb; ++j) {
-        r = fmaf(b[j], __ldg(sh + 3 * j + 0), r);
-        g = fmaf(b[j], __ldg(sh + 3 * j + 1), g);
-        bl = fmaf(b[j], __ldg(sh + 3 * j + 2), bl);
+    if (deg == 3) {   // 48 coefficients = 12 aligned float4 loads (sh is 16-byte aligned)
+        float c[48];
+        const float4 *s4 = reinterpret_cast<const float4 *>(sh);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            const float4 v = __ldg(s4 + k);
+            c[4 * k] = v.x; c[4 * k + 1] = v.y; c[4 * k + 2] = v.z; c[4 * k + 3] = v.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            r = fmaf(b[j], c[3 * j + 0], r);
+            g = fmaf(b[j], c[3 * j + 1], g);
+            bl = fmaf(b[j], c[3 * j + 2], bl);
+        }
+    } else {
+        for (int j = 0; j < nb; ++j) {
+            r = fmaf(b[j], __ldg(sh + 3 * j + 0), r);
+            g = fmaf(b[j], __ldg(sh + 3 * j + 1), g);
+            bl = fmaf(b[j], __ldg(sh + 3 * j + 2), bl);
+        }
     }
     rgb[0] = fmaxf(r + 0.5f, 0.f);
     rgb[1] = fmaxf(g + 0.5f, 0.f);
@@ -265,15 +283,131 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
     }
 }
 
+// ------------------------------------------------------------------ cull
+// Conservative cull ahead of the fp64 projection: a surfel is dropped when
+// its centre fails the depth-key test (exact, the same pinned key as
+// k_project) or when the sphere of radius 3.001 max(s_u, s_v) around its
+// sensor-frame centre (which holds the 3-sigma support disk) lies outside
+// the sensor's field of view widened by a margin (pinhole: 4 px beyond the
+// image, covering the low-pass disc; fisheye: 0.15 rad beyond theta_max;
+// LiDAR: 1e-4 rad beyond the beam fan).  fp32 arithmetic with margins well
+// above its error; only used to skip work -- k_project takes every decision
+// for the surfels that pass.  Passing surfels are compacted in index order
+// (decoupled look-back); the others get the culled outputs here.
+template <int KIND>
+__device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op, int64_t i,
+                                         uint32_t &keybits) {
+    const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1), mz = __ldg(s.means + 3 * i + 2);
+    float keyf;
+    if (KIND == GS_PINHOLE) {
+        keyf = (float)pinned_row(se.R + 6, se.t[2], mx, my, mz);
+    } else {
+        const double a = pinned_row(se.R + 0, se.t[0], mx, my, mz);
+        const double b = pinned_row(se.R + 3, se.t[1], mx, my, mz);
+        const double c = pinned_row(se.R + 6, se.t[2], mx, my, mz);
+        keyf = (float)__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
+    }
+    keybits = __float_as_uint(keyf);
+    const float o = __ldg(s.opac + i);
+    const float2 sc = __ldg(reinterpret_cast<const float2 *>(s.scales) + i);
+    if (!(keyf >= op.near_plane) || !(o > 0.f) || !(sc.x > 0.f) || !(sc.y > 0.f) || !isfinite(sc.x) ||
+        !isfinite(sc.y))
+        return false;
+    const float X = fmaf(se.R[0], mx, fmaf(se.R[1], my, fmaf(se.R[2], mz, se.t[0])));
+    const float Y = fmaf(se.R[3], mx, fmaf(se.R[4], my, fmaf(se.R[5], mz, se.t[1])));
+    const float Z = fmaf(se.R[6], mx, fmaf(se.R[7], my, fmaf(se.R[8], mz, se.t[2])));
+    const float R = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f) * fmaxf(sc.x, sc.y) +
+                    1e-3f * (1.f + fabsf(X) + fabsf(Y) + fabsf(Z));
+    if (!isfinite(X + Y + Z + R)) return true;   // let k_project decide
+    if (KIND == GS_PINHOLE) {
+        const float m = 4.f;
+        const float xl = (-m - se.cx) / se.fx, xr = ((float)se.width + m - se.cx) / se.fx;
+        const float yl = (-m - se.cy) / se.fy, yr = ((float)se.height + m - se.cy) / se.fy;
+        if ((X - xl * Z) < -R * sqrtf(1.f + xl * xl)) return false;
+        if ((xr * Z - X) < -R * sqrtf(1.f + xr * xr)) return false;
+        if ((Y - yl * Z) < -R * sqrtf(1.f + yl * yl)) return false;
+        if ((yr * Z - Y) < -R * sqrtf(1.f + yr * yr)) return false;
+        return true;
+    }
+    const float r = sqrtf(X * X + Y * Y + Z * Z);
+    if (!(r > R * 1.01f)) return true;
+    const float beta = asinf(R / r);
+    if (KIND == GS_FISHEYE_EQUIDISTANT) {
+        const float th = acosf(fminf(1.f, fmaxf(-1.f, Z / r)));
+        return th - beta <= se.theta_max + 0.15f;
+    }
+    const float el = asinf(fminf(1.f, fmaxf(-1.f, Z / r)));
+    const float top = se.beam[0], bot = se.beam[se.nbeams - 1];
+    return el + beta >= bot - 1e-4f && el - beta <= top + 1e-4f;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __grid_constant__ DevSensor se,
+                                                       DevOpts op, short4 *__restrict__ rect,
+                                                       uint32_t *__restrict__ keys, uint32_t *__restrict__ counts,
+                                                       uint32_t *__restrict__ cand, unsigned long long *st_cand,
+                                                       ProjHeader *hdr) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_w[SCAN_THREADS / 32], s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->cull_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // item j of thread t: base + j * SCAN_THREADS + t (coalesced); ranks in index order via per-round ballots
+    const int64_t base = (int64_t)tile * SCAN_TILE;
+    uint32_t flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+        if (i < s.n) {
+            uint32_t kb;
+            const bool c = cull_one<KIND>(s, se, op, i, kb);
+            if (c) { flags |= 1u << j; ++cnt; }
+            else {
+                keys[i] = 0xffffffffu;
+                counts[i] = 0;
+                rect[i] = make_short4(0, 0, -1, -1);
+            }
+        }
+    }
+    // per round j: CTA-wide exclusive rank of this thread's item among the passing items of round j
+    __shared__ uint32_t s_round[SCAN_ITEMS][SCAN_THREADS / 32];
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const uint32_t b = __ballot_sync(FULL_MASK, (flags >> j) & 1u);
+        if (lane == 0) s_round[j][warp] = __popc(b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int j = 0; j < SCAN_ITEMS; ++j)
+            for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+                const uint32_t c = s_round[j][w];
+                s_round[j][w] = (uint32_t)tot;
+                tot += c;
+            }
+        const unsigned long long e = lookback_u64(st_cand, tile, tot);
+        s_excl = e;
+        if (base + SCAN_TILE >= s.n) hdr->n_cand = (uint32_t)(e + tot);
+    }
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const uint32_t b = __ballot_sync(FULL_MASK, (flags >> j) & 1u);
+        if ((flags >> j) & 1u) {
+            const unsigned long long pos = s_excl + s_round[j][warp] + __popc(b & lt);
+            cand[pos] = (uint32_t)(base + j * SCAN_THREADS + threadIdx.x);
+        }
+    }
+    (void)cnt;
+}
+
 // ------------------------------------------------------------------ projection
 template <int KIND>
-__global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_constant__ DevSensor se,
-                                                 DevOpts op, float *__restrict__ rec,
-                                                 short4 *__restrict__ rect,
-                                                 uint32_t *__restrict__ keys,
-                                                 uint32_t *__restrict__ counts) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= s.n) return;
+__device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op,
+                                            int64_t i, float *__restrict__ rec, short4 *__restrict__ rect,
+                                            uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
     const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1),
                 mz = __ldg(s.means + 3 * i + 2);
     double mu[3];
@@ -539,13 +673,26 @@ __global__ void __launch_bounds__(256) k_project(DevSurfels s, const __grid_cons
     }
 }
 
+// One thread per candidate (grid-stride over the compacted list of k_cull).
+template <int KIND>
+__global__ void __launch_bounds__(256, 2) k_project(DevSurfels s, const __grid_constant__ DevSensor se, DevOpts op,
+                                                 const uint32_t *__restrict__ cand, const ProjHeader *hdr,
+                                                 float *__restrict__ rec, short4 *__restrict__ rect,
+                                                 uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
+    const uint32_t nc = hdr->n_cand;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
+        project_one<KIND>(s, se, op, (int64_t)cand[c], rec, rect, keys, counts);
+}
+
 // ------------------------------------------------------------------ compaction
-// Visible surfels (count > 0) in index order -> (vis_key, vis_id); totals of
-// visible surfels and of pairs -> header and d_num_pairs.  One CTA = 2048
-// surfels; each lane owns 8 consecutive surfels; decoupled look-back.
+// Visible surfels (count > 0) among the candidates, in index order ->
+// (vis_key, vis_id); totals of visible surfels and of pairs -> header and
+// d_num_pairs.  One CTA = 2048 candidates; each lane owns 8 consecutive
+// candidates; decoupled look-back.
 __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__restrict__ keys,
                                                           const uint32_t *__restrict__ counts,
-                                                          int64_t n, uint32_t *__restrict__ vkey,
+                                                          const uint32_t *__restrict__ cand,
+                                                          uint32_t *__restrict__ vkey,
                                                           uint32_t *__restrict__ vid,
                                                           unsigned long long *st_vis,
                                                           unsigned long long *st_pairs,
@@ -556,14 +703,17 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->scan_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
+    const int64_t n = hdr->n_cand;
+    if ((int64_t)tile * SCAN_TILE >= n && tile > 0) return;   // beyond the candidates: nobody looks back here
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)(warp * 32 + lane) * SCAN_ITEMS;
-    uint32_t c[SCAN_ITEMS];
+    uint32_t c[SCAN_ITEMS], id[SCAN_ITEMS];
     uint32_t lv = 0, lp = 0;
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const int64_t idx = base + j;
-        c[j] = idx < n ? counts[idx] : 0u;
+        id[j] = idx < n ? cand[idx] : 0u;
+        c[j] = idx < n ? counts[id[j]] : 0u;
         lv += c[j] > 0 ? 1u : 0u;
         lp += c[j];
     }
@@ -595,21 +745,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const int64_t idx = base + j;
         if (c[j] > 0) {
-            vkey[pos] = keys[idx];
-            vid[pos] = (uint32_t)idx;
+            vkey[pos] = keys[id[j]];
+            vid[pos] = id[j];
             ++pos;
         }
     }
 }
-
-template __global__ void k_project<GS_PINHOLE>(DevSurfels, const __grid_constant__ DevSensor, DevOpts,
-                                               float *, short4 *, uint32_t *, uint32_t *);
-template __global__ void k_project<GS_FISHEYE_EQUIDISTANT>(DevSurfels, const __grid_constant__ DevSensor,
-                                                           DevOpts, float *, short4 *, uint32_t *,
-                                                           uint32_t *);
-template __global__ void k_project<GS_LIDAR_SPINNING>(DevSurfels, const __grid_constant__ DevSensor,
-                                                      DevOpts, float *, short4 *, uint32_t *,
-                                                      uint32_t *);
 
 // host-side launchers (called from abi.cu)
 cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOpts &op, void *proj,
@@ -619,30 +760,38 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     ProjHeader *hdr = (ProjHeader *)base;
     cudaError_t e = cudaMemsetAsync(hdr, 0, sizeof(ProjHeader), st);
     if (e != cudaSuccess) return e;
-    const size_t nblk = ((size_t)s.n + SCAN_TILE - 1) / SCAN_TILE;
-    e = cudaMemsetAsync(base + L.status, 0, 2 * (nblk + 1) * 8, st);
+    e = cudaMemsetAsync(base + L.status, 0, 3 * (L.nblk + 1) * 8, st);
     if (e != cudaSuccess) return e;
     if (s.n == 0) {
         if (d_num_pairs) return cudaMemsetAsync(d_num_pairs, 0, 8, st);
         return cudaSuccess;
     }
-    const unsigned grid = (unsigned)((s.n + 255) / 256);
     float *rec = (float *)(base + L.rec);
     short4 *rect = (short4 *)(base + L.rect);
     uint32_t *key = (uint32_t *)(base + L.key), *cnt = (uint32_t *)(base + L.cnt);
-    if (se.kind == GS_PINHOLE)
-        k_project<GS_PINHOLE><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
-    else if (se.kind == GS_FISHEYE_EQUIDISTANT)
-        k_project<GS_FISHEYE_EQUIDISTANT><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
-    else
-        k_project<GS_LIDAR_SPINNING><<<grid, 256, 0, st>>>(s, se, op, rec, rect, key, cnt);
-    note_launch(2);   // k_project + k_compact
+    uint32_t *cand = (uint32_t *)(base + L.cand);
+    unsigned long long *stv = (unsigned long long *)(base + L.status);
+    unsigned long long *stp = stv + L.nblk + 1, *stc = stp + L.nblk + 1;
+    const unsigned nblk = (unsigned)L.nblk;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * 8);
+    note_launch(3);   // k_cull + k_project + k_compact
+    if (se.kind == GS_PINHOLE) {
+        k_cull<GS_PINHOLE><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
+        k_project<GS_PINHOLE><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
+    } else if (se.kind == GS_FISHEYE_EQUIDISTANT) {
+        k_cull<GS_FISHEYE_EQUIDISTANT><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
+        k_project<GS_FISHEYE_EQUIDISTANT><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
+    } else {
+        k_cull<GS_LIDAR_SPINNING><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
+        k_project<GS_LIDAR_SPINNING><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    unsigned long long *stv = (unsigned long long *)(base + L.status);
-    k_compact<<<(unsigned)nblk, SCAN_THREADS, 0, st>>>(key, cnt, s.n, (uint32_t *)(base + L.vkey),
-                                                      (uint32_t *)(base + L.vid), stv, stv + nblk + 1,
-                                                      hdr, d_num_pairs);
+    k_compact<<<nblk, SCAN_THREADS, 0, st>>>(key, cnt, cand, (uint32_t *)(base + L.vkey), (uint32_t *)(base + L.vid),
+                                            stv, stp, hdr, d_num_pairs);
     return cudaGetLastError();
 }
 

@@ -5,15 +5,21 @@
 // low-pass floor for cameras; north_star rule alpha = min(alpha_max,
 // o G), skip alpha < alpha_min, stop before T < t_min.
 //
-// Work decomposition (B200): a tile is the 32 samples of ONE warp (8x4
-// pixels, or 32 LiDAR columns of one beam).  Warps are persistent: they pull
-// work items from a longest-first schedule built on the device, stage their
-// tile's depth-sorted surfel records into warp-private shared memory with
-// cp.async (32 records per batch, double buffered) and walk them in order.
-// Lists longer than split_len are cut into segments that run in parallel; a
-// merge kernel combines the segment composites with the transmittance prefix
-// and re-walks the one segment in which a ray stops, so the stop rule stays
-// exact.  No atomics touch the outputs: results are bitwise deterministic.
+// Work decomposition (B200): one CTA composites one binning
+// tile (opts tile_w x tile_h samples); each of its warps owns a 32-sample
+// sub-tile (8x4 pixels for cameras, 32x1 LiDAR columns of one beam).  The CTA
+// stages its tile's depth-sorted surfel records into shared memory with
+// cp.async, one record per thread per batch (double buffered), so every
+// record is fetched from L2/HBM once per tile; each warp then ballots which
+// records of the batch touch its sub-tile (conservative pixel box) and walks
+// only those, in list order, with warp-vote early termination.  CTAs are
+// persistent and pull work items (tile, segment) from a longest-first
+// schedule built on the device.  Lists longer than split_len are cut into
+// segments composited in parallel; a merge kernel combines the segment
+// composites with the transmittance prefix and re-walks the one segment in
+// which a ray stops, so the stop rule stays exact.  No atomics touch the
+// outputs: results are bitwise deterministic and, for unsplit lists,
+// independent of the tile shape.
 //
 // The plane pair of a sample meets the surfel where
 // (M^T h_u) x (M^T h_v) = det(M) M^{-1} (h_u x h_v): the kernels evaluate the
@@ -44,10 +50,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr float LOG2E_HALF = 0.72134752044448170368f;   // 0.5 * log2(e)
-constexpr int WARPS = 8;                                 // warps per CTA
 constexpr int NB = 32;                                   // schedule buckets
 constexpr int NPART = 10;                                // floats per partial composite
-constexpr uint32_t DEFAULT_SPLIT = 2048;
+constexpr uint32_t LMIN = 1024;   // shortest segment of the adaptive split (workspace sizing)
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int KIND> struct Rec;
 template <> struct Rec<GS_PINHOLE> { static constexpr int F = PH_FLOATS, BB = PH_BBX; };
@@ -60,8 +66,10 @@ struct SchedHdr {
     uint32_t n_items;
     uint32_t n_split;        // tiles whose list was split
     uint32_t slot_cursor;    // partial-slot allocator
-    uint32_t seg_len;        // segment length L in use
-    uint32_t pad0[3];
+    uint32_t rw_count;       // re-walk items (split tile, segment) appended by k_merge_plan
+    uint32_t rw_counter;     // persistent work counter of k_rewalk
+    uint32_t P;              // total pairs (max tile range end)
+    uint32_t pad0;
     uint32_t bucket_cnt[NB];
     uint32_t bucket_cur[NB];
     uint32_t pad1[24];
@@ -69,10 +77,10 @@ struct SchedHdr {
 static_assert(sizeof(SchedHdr) == 384, "hdr");
 
 struct RenderWs {
-    size_t hdr, items, split_base, split_list, partials, total;
+    size_t hdr, items, split_base, split_list, partials, mstate, rw_items, total;
     uint32_t max_items, max_split, max_slots, L;
-    RenderWs(int64_t cap, int64_t ntiles, int32_t split_len) {
-        L = split_len > 0 ? (uint32_t)split_len : DEFAULT_SPLIT;
+    RenderWs(int64_t cap, int64_t ntiles, int32_t split_len, int npix) {
+        L = split_len > 0 ? (uint32_t)split_len : LMIN;
         const uint64_t c = (uint64_t)(cap > 0 ? cap : 0);
         max_items = (uint32_t)(ntiles + c / L + 1);
         max_split = (uint32_t)std::min<uint64_t>((uint64_t)ntiles, c / L + 1);
@@ -82,7 +90,9 @@ struct RenderWs {
         items = o; o += align256((size_t)max_items * 8);
         split_base = o; o += align256((size_t)ntiles * 4);
         split_list = o; o += align256((size_t)max_split * 4);
-        partials = o; o += align256((size_t)max_slots * 32 * NPART * 4);
+        partials = o; o += align256((size_t)max_slots * NPART * npix * 4);
+        mstate = o; o += align256((size_t)max_split * NPART * npix * 4);
+        rw_items = o; o += align256((size_t)max_slots * 8);
         total = o;
     }
 };
@@ -99,15 +109,32 @@ struct Acc {
     float T, A, c0, c1, c2, d, n0, n1, n2;
 };
 
-template <int KIND>
-__device__ __forceinline__ Ray make_ray(const DevSensor &se, int tile, int lane) {
-    Ray ry;
+// The 32 samples of one warp: an sw x sh block of its tile (compact sub-tiles
+// keep small surfels inside few warps; measured faster than interleaving the
+// warps' rows, which balances the warps of a tile but spreads each surfel
+// over more of them).
+struct SubTile {
+    int x0, y0, x1, y1;   // inclusive
+};
+
+__device__ __forceinline__ SubTile sub_tile(const DevSensor &se, int tile, int warp) {
     const int tyi = tile / se.ntx, txi = tile - tyi * se.ntx;
-    const int lx = lane % se.tw, ly = lane / se.tw;
-    ry.pxi = txi * se.tw + lx;
-    ry.pyi = tyi * se.th + ly;
+    const int nsx = se.tw / se.sw;
+    SubTile st;
+    st.x0 = txi * se.tw + (warp % nsx) * se.sw;
+    st.y0 = tyi * se.th + (warp / nsx) * se.sh;
+    st.x1 = st.x0 + se.sw - 1;
+    st.y1 = st.y0 + se.sh - 1;
+    return st;
+}
+
+template <int KIND>
+__device__ __forceinline__ Ray make_ray(const DevSensor &se, const SubTile &st, int lane) {
+    Ray ry;
+    ry.pxi = st.x0 + lane % se.sw;
+    ry.pyi = st.y0 + lane / se.sw;
     ry.pxw = ry.pxi + se.width;
-    ry.inside = lane < se.tw * se.th && ry.pxi < se.width && ry.pyi < se.height;
+    ry.inside = ry.pxi < se.width && ry.pyi < se.height;
     ry.px = (float)ry.pxi + 0.5f;
     ry.py = (float)ry.pyi + 0.5f;
     ry.valid = ry.inside;
@@ -129,21 +156,21 @@ __device__ __forceinline__ Ray make_ray(const DevSensor &se, int tile, int lane)
         }
         double sp = 0.0, cp = 1.0;
         if (td > 0.0) { cp = mx / td; sp = my / td; }
-        double st, ct;
-        sincos(th, &st, &ct);
-        split_hilo(st * cp, ry.dh[0], ry.dl[0]);
-        split_hilo(st * sp, ry.dh[1], ry.dl[1]);
+        double st_, ct;
+        sincos(th, &st_, &ct);
+        split_hilo(st_ * cp, ry.dh[0], ry.dl[0]);
+        split_hilo(st_ * sp, ry.dh[1], ry.dl[1]);
         split_hilo(ct, ry.dh[2], ry.dl[2]);
     }
     if (KIND == GS_LIDAR_SPINNING && ry.inside) {   // Eq. 5: theta = elevation (row), phi = azimuth (column)
         const double th = (double)se.beam[ry.pyi];
         const double ph = (double)se.az0 + (double)ry.pxi * (double)se.az_step;
-        double st, ct, sf, cf;
-        sincos(th, &st, &ct);
+        double st_, ct, sf, cf;
+        sincos(th, &st_, &ct);
         sincos(ph, &sf, &cf);
         split_hilo(ct * cf, ry.dh[0], ry.dl[0]);
         split_hilo(ct * sf, ry.dh[1], ry.dl[1]);
-        split_hilo(st, ry.dh[2], ry.dl[2]);
+        split_hilo(st_, ry.dh[2], ry.dl[2]);
     }
     return ry;
 }
@@ -154,6 +181,15 @@ __device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int x, int xw, 
     const uint32_t wx = (uint32_t)(x1 - x0);
     const bool okx = (uint32_t)(x - x0) <= wx || (uint32_t)(xw - x0) <= wx;
     return okx && (uint32_t)(y - y0) <= (uint32_t)(y1 - y0);
+}
+
+// Does a record's conservative pixel box (packed u16 pairs; LiDAR columns may
+// run past width-1 = azimuth wrap) touch the sub-tile?
+__device__ __forceinline__ bool box_hits(uint32_t bx, uint32_t by, const SubTile &st, int W) {
+    const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
+    const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
+    const bool okx = (x0 <= st.x1 && x1 >= st.x0) || (x0 <= st.x1 + W && x1 >= st.x0 + W);
+    return okx && y0 <= st.y1 && y1 >= st.y0;
 }
 
 // One (sample, surfel) evaluation in list order.  Returns false once the ray
@@ -233,55 +269,70 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
     return true;
 }
 
-// Walk list entries [s, e) of `values` for the 32 lanes of this warp.
-// wbuf: warp-private shared memory, 2 x 32 records.  `done` lanes skip work;
-// a lane becomes done when its ray stops.  Returns true if the ray stopped.
+// CTA walk of list entries [s, e) of `values`; every thread of the CTA calls
+// it (it holds barriers).  smem: 2 x blockDim records.  Each thread's sample
+// is `ry` in its warp's sub-tile `st`; `done` lanes skip work and a lane
+// becomes done when its ray stops (`stopped`).
 template <int KIND, bool STATS>
 __device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
-                                     uint32_t s, uint32_t e, float4 *wbuf, const Ray &ry,
-                                     const DevOpts &op, Acc &a, bool &done, bool &stopped,
+                                     uint32_t s, uint32_t e, float4 *smem, const SubTile &st, const Ray &ry,
+                                     const DevSensor &se, const DevOpts &op, Acc &a, bool &done, bool &stopped,
                                      uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4;
-    const int lane = threadIdx.x & 31;
-    if (__all_sync(0xffffffffu, done) || s >= e) return;
+    constexpr int BB4 = Rec<KIND>::BB / 4;
+    const int B = blockDim.x, t = threadIdx.x, lane = t & 31;
+    bool wdone = __all_sync(FULL, done);
+    if (__syncthreads_count(!wdone) == 0 || s >= e) return;
     auto stage = [&](uint32_t first, float4 *dst) {
-        if (first + lane < e) {
-            const uint32_t id = __ldg(values + first + lane);
+        if (first + t < e) {
+            const uint32_t id = __ldg(values + first + t);
             const float4 *src = rec + (size_t)id * R4;
-            float4 *d = dst + lane * R4;
+            float4 *d = dst + t * R4;
 #pragma unroll
             for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
         }
         cp_async_commit();
     };
-    const uint32_t nb = (e - s + 31) >> 5;
-    stage(s, wbuf);
+    const uint32_t nb = (e - s + B - 1) / B;
+    stage(s, smem);
     for (uint32_t b = 0; b < nb; ++b) {
         if (b + 1 < nb) {
-            stage(s + (b + 1) * 32, wbuf + ((b + 1) & 1) * 32 * R4);
+            stage(s + (b + 1) * B, smem + ((b + 1) & 1) * B * R4);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncwarp();
-        const float4 *buf = wbuf + (b & 1) * 32 * R4;
-        const int cnt = (int)min(32u, e - (s + b * 32));
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                if (!eval_record<KIND, STATS>(buf + j * R4, ry, op, a, n_eval, n_comp)) {
-                    done = true;
-                    stopped = true;
-                    break;
+        __syncthreads();
+        const float4 *buf = smem + (b & 1) * B * R4;
+        const int cnt = (int)min((uint32_t)B, e - (s + b * B));
+        if (!wdone) {
+            for (int c = 0; c < cnt; c += 32) {
+                bool hit = false;
+                if (c + lane < cnt) {
+                    const float4 bb = buf[(c + lane) * R4 + BB4];
+                    hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
                 }
+                uint32_t bits = __ballot_sync(FULL, hit);
+                if (!bits) continue;
+                if (!done) {
+                    do {
+                        const int j = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        if (!eval_record<KIND, STATS>(buf + (c + j) * R4, ry, op, a, n_eval, n_comp)) {
+                            done = true;
+                            stopped = true;
+                            break;
+                        }
+                    } while (bits);
+                }
+                if (__all_sync(FULL, done)) { wdone = true; break; }
             }
         }
-        if (__all_sync(0xffffffffu, done)) {
-            cp_async_wait<0>();
-            __syncwarp();
-            return;
-        }
-        __syncwarp();
+        // every warp is past batch b (its buffer may be restaged); stop once all warps are done
+        if (__syncthreads_count(!wdone) == 0) break;
     }
+    cp_async_wait<0>();
+    __syncthreads();
 }
 
 template <int KIND>
@@ -321,9 +372,26 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t len, uint32_t L) {
     return b >= NB ? NB - 1 : b;
 }
 
+// Segment length: fixed (opts split_len > 0), else adaptive -- about half a
+// fair share of the frame's pairs per resident CTA (at least LMIN), so the
+// longest-first schedule keeps every SM busy to the end.
+__device__ __forceinline__ uint32_t seg_len(const SchedHdr *h, uint32_t lfix, uint32_t ctas) {
+    if (lfix) return lfix;
+    const uint32_t share = (h->P / (2u * ctas) + 255u) & ~255u;
+    return share > LMIN ? share : LMIN;
+}
+
 // ---------------------------------------------------------------- schedule
+__global__ void k_sched_total(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow, SchedHdr *h) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles || (d_overflow && *d_overflow)) return;
+    const uint32_t e = ranges[t].y;
+    if (e) atomicMax(&h->P, e);
+}
+
 __global__ void k_sched_count(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow,
-                              SchedHdr *h, uint32_t L) {
+                              SchedHdr *h, uint32_t lfix, uint32_t ctas) {
+    const uint32_t L = seg_len(h, lfix, ctas);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
     const bool ovf = d_overflow && *d_overflow;
@@ -338,7 +406,7 @@ __global__ void k_sched_scan(SchedHdr *h) {   // one warp: descending-bucket exc
     uint32_t x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
         if (lane >= o) x += y;
     }
     h->bucket_cur[NB - 1 - lane] = x - c;
@@ -347,7 +415,8 @@ __global__ void k_sched_scan(SchedHdr *h) {   // one warp: descending-bucket exc
 
 __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow,
                              SchedHdr *h, uint2 *__restrict__ items, uint32_t *__restrict__ split_base,
-                             uint32_t *__restrict__ split_list, uint32_t L) {
+                             uint32_t *__restrict__ split_list, uint32_t lfix, uint32_t ctas) {
+    const uint32_t L = seg_len(h, lfix, ctas);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
     const bool ovf = d_overflow && *d_overflow;
@@ -363,24 +432,28 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 }
 
 // ---------------------------------------------------------------- composite
+// Persistent CTAs (blockDim = samples per tile); one work item = (tile,
+// segment).  Unsplit tiles are written out; segments of split tiles leave
+// their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
-__global__ void __launch_bounds__(WARPS * 32) k_render(
+__global__ void __launch_bounds__(512) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ o0, float *__restrict__ o1,
-    float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t L) {
-    constexpr int R4 = Rec<KIND>::F / 4;
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
+    const uint32_t L = seg_len(h, lfix, ctas);
     extern __shared__ float4 smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4 *wbuf = smem + warp * 2 * 32 * R4;
+    __shared__ uint32_t s_item;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
     const bool ovf = d_overflow && *d_overflow;
     const uint32_t n_items = h->n_items;
     while (true) {
-        uint32_t item = 0;
-        if (lane == 0) item = atomicAdd(&h->counter, 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
+        if (t == 0) s_item = atomicAdd(&h->counter, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        __syncthreads();
         if (item >= n_items) break;
         const uint2 it = items[item];
         const int tile = (int)it.x;
@@ -389,11 +462,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_render(
         if (ovf) rg.y = rg.x;
         const uint32_t len = rg.y - rg.x, ns = seg_count(len, L);
         const uint32_t s = rg.x + seg * L, e = min(rg.y, s + L);
-        const Ray ry = make_ray<KIND>(se, tile, lane);
+        const SubTile st = sub_tile(se, tile, warp);
+        const Ray ry = make_ray<KIND>(se, st, lane);
         Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !ry.valid, stopped = false;
         uint32_t n_eval = 0, n_comp = 0;
-        walk<KIND, STATS>(rec, values, s, e, wbuf, ry, op, a, done, stopped, n_eval, n_comp);
+        walk<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, n_eval, n_comp);
         if (ns == 1) {
             write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
             if (STATS && ry.inside) {
@@ -402,99 +476,117 @@ __global__ void __launch_bounds__(WARPS * 32) k_render(
                 out_stats[HW + pix] = n_eval;
             }
         } else {
-            float *p = partials + ((size_t)(split_base[tile] + seg) * 32 + lane) * NPART;
-            p[0] = a.T; p[1] = a.A; p[2] = a.c0; p[3] = a.c1; p[4] = a.c2;
-            p[5] = a.d; p[6] = a.n0; p[7] = a.n1; p[8] = a.n2; p[9] = stopped ? 1.f : 0.f;
+            float *p = partials + (size_t)(split_base[tile] + seg) * NPART * npix + t;
+            p[0 * npix] = a.T; p[1 * npix] = a.A; p[2 * npix] = a.c0; p[3 * npix] = a.c1;
+            p[4 * npix] = a.c2; p[5 * npix] = a.d; p[6 * npix] = a.n0; p[7 * npix] = a.n1;
+            p[8 * npix] = a.n2; p[9 * npix] = stopped ? 1.f : 0.f;
         }
     }
 }
 
 // ---------------------------------------------------------------- merge of split lists
-// One CTA per split tile.  Warp 0 walks the segment composites in order,
-// C += T_run C_k, T_run *= T_k, while no stop can have happened
-// (no local stop and T_run T_k >= t_min); the first segment in which a ray
-// stops with T_run < 1 is re-walked from T_run with the exact stop rule (the
-// 8 warps share the distinct re-walk segments).
+// k_merge_plan: one CTA per split tile, one thread per sample.  Each sample
+// walks its segment composites in order, C += T_run C_k, T_run *= T_k, while
+// no stop can have happened (no local stop and T_run T_k >= t_min).  Samples
+// that never stop inside a later segment are final and written out; for the
+// others the first segment k* in which the ray stops with T_run < 1 must be
+// re-walked from T_run with the exact stop rule: their prefix composite and
+// k* are kept in `mstate` (SoA) and one re-walk item (split tile, k*) is
+// appended per distinct k*.  k_rewalk then walks those items in parallel.
 template <int KIND>
-__global__ void __launch_bounds__(WARPS * 32) k_merge(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+__global__ void __launch_bounds__(512) k_merge_plan(
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
-    const SchedHdr *h, const uint32_t *__restrict__ split_base, const uint32_t *__restrict__ split_list,
-    const float *__restrict__ partials, float *__restrict__ o0, float *__restrict__ o1,
-    float *__restrict__ o2, float *__restrict__ o3, uint32_t L) {
-    constexpr int R4 = Rec<KIND>::F / 4;
-    extern __shared__ float4 smem[];
-    __shared__ int s_k[32];
-    __shared__ float s_T[32];
-    __shared__ Acc s_acc[32], s_re[32];
+    SchedHdr *h, const uint32_t *__restrict__ split_base, const uint32_t *__restrict__ split_list,
+    const float *__restrict__ partials, float *__restrict__ mstate, uint2 *__restrict__ rw_items,
+    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
+    const uint32_t L = seg_len(h, lfix, ctas);
     if (blockIdx.x >= h->n_split) return;
     const int tile = (int)split_list[blockIdx.x];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
     const uint2 rg = ranges[tile];
     const uint32_t ns = seg_count(rg.y - rg.x, L), base = split_base[tile];
-    const Ray ry = make_ray<KIND>(se, tile, lane);
-    if (warp == 0) {
-        Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        int kstar = -1;
-        for (uint32_t k = 0; k < ns; ++k) {
-            const float *p = partials + ((size_t)(base + k) * 32 + lane) * NPART;
-            const float Tk = p[0];
-            const bool stop_k = p[9] != 0.f;
-            if (!stop_k && a.T * Tk >= op.t_min) {
-                const float Tr = a.T;
-                a.A = fmaf(Tr, p[1], a.A); a.c0 = fmaf(Tr, p[2], a.c0); a.c1 = fmaf(Tr, p[3], a.c1);
-                a.c2 = fmaf(Tr, p[4], a.c2); a.d = fmaf(Tr, p[5], a.d); a.n0 = fmaf(Tr, p[6], a.n0);
-                a.n1 = fmaf(Tr, p[7], a.n1); a.n2 = fmaf(Tr, p[8], a.n2);
-                a.T = Tr * Tk;
-            } else if (a.T == 1.f) {   // nothing composited before: the local composite is exact
-                a.T = Tk; a.A = p[1]; a.c0 = p[2]; a.c1 = p[3]; a.c2 = p[4];
-                a.d = p[5]; a.n0 = p[6]; a.n1 = p[7]; a.n2 = p[8];
-                break;
-            } else {
-                kstar = (int)k;
-                break;
-            }
+    const SubTile st = sub_tile(se, tile, warp);
+    const Ray ry = make_ray<KIND>(se, st, lane);
+    Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int kstar = -1;
+    for (uint32_t k = 0; k < ns; ++k) {
+        const float *p = partials + (size_t)(base + k) * NPART * npix + t;
+        const float Tk = p[0];
+        const bool stop_k = p[9 * npix] != 0.f;
+        if (!stop_k && a.T * Tk >= op.t_min) {
+            const float Tr = a.T;
+            a.A = fmaf(Tr, p[1 * npix], a.A); a.c0 = fmaf(Tr, p[2 * npix], a.c0);
+            a.c1 = fmaf(Tr, p[3 * npix], a.c1); a.c2 = fmaf(Tr, p[4 * npix], a.c2);
+            a.d = fmaf(Tr, p[5 * npix], a.d); a.n0 = fmaf(Tr, p[6 * npix], a.n0);
+            a.n1 = fmaf(Tr, p[7 * npix], a.n1); a.n2 = fmaf(Tr, p[8 * npix], a.n2);
+            a.T = Tr * Tk;
+        } else if (a.T == 1.f) {   // nothing composited before: the local composite is exact
+            a.T = Tk; a.A = p[1 * npix]; a.c0 = p[2 * npix]; a.c1 = p[3 * npix]; a.c2 = p[4 * npix];
+            a.d = p[5 * npix]; a.n0 = p[6 * npix]; a.n1 = p[7 * npix]; a.n2 = p[8 * npix];
+            break;
+        } else {
+            kstar = (int)k;
+            break;
         }
-        s_k[lane] = ry.valid ? kstar : -1;
-        s_T[lane] = a.T;
-        s_acc[lane] = a;
-        s_re[lane] = Acc{a.T, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     }
-    __syncthreads();
-    // distinct re-walk segments, dealt round-robin to the warps
-    int nd = 0;
-    for (int i = 0; i < 32; ++i) {
-        const int k = s_k[i];
-        if (k < 0) continue;
-        bool first = true;
-        for (int j = 0; j < i; ++j) first = first && (s_k[j] != k);
-        if (!first) continue;
-        if (nd % WARPS == warp) {
-            const bool mine = s_k[lane] == k;
-            Acc a = {s_T[lane], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            bool done = !mine, stopped = false;
-            uint32_t ne = 0, nc = 0;
-            const uint32_t s = rg.x + (uint32_t)k * L, e = min(rg.y, s + L);
-            walk<KIND, false>(rec, values, s, e, smem + warp * 2 * 32 * R4, ry, op, a, done, stopped, ne, nc);
-            if (mine) s_re[lane] = a;
-        }
-        ++nd;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        Acc a = s_acc[lane];
-        const Acc r = s_re[lane];
-        if (s_k[lane] >= 0) {
-            a.T = r.T; a.A += r.A; a.c0 += r.c0; a.c1 += r.c1; a.c2 += r.c2;
-            a.d += r.d; a.n0 += r.n0; a.n1 += r.n1; a.n2 += r.n2;
-        }
+    if (!ry.valid) kstar = -1;
+    if (kstar < 0) {
         write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
+    }
+    float *m = mstate + (size_t)blockIdx.x * NPART * npix + t;
+    m[0 * npix] = a.T; m[1 * npix] = a.A; m[2 * npix] = a.c0; m[3 * npix] = a.c1; m[4 * npix] = a.c2;
+    m[5 * npix] = a.d; m[6 * npix] = a.n0; m[7 * npix] = a.n1; m[8 * npix] = a.n2;
+    m[9 * npix] = __int_as_float(kstar);
+    for (uint32_t k = 0; k < ns; ++k)
+        if (__syncthreads_or(kstar == (int)k) && t == 0)
+            rw_items[atomicAdd(&h->rw_count, 1u)] = make_uint2(blockIdx.x, k);
+}
+
+// Persistent CTAs over the re-walk items: segment k of split tile s is walked
+// from each stopping sample's prefix transmittance; the segment's result is
+// added to the prefix composite and the sample written out.
+template <int KIND>
+__global__ void __launch_bounds__(512) k_rewalk(
+    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
+    SchedHdr *h, const uint32_t *__restrict__ split_list, const float *__restrict__ mstate,
+    const uint2 *__restrict__ rw_items, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
+    const uint32_t L = seg_len(h, lfix, ctas);
+    extern __shared__ float4 smem[];
+    __shared__ uint32_t s_item;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
+    const uint32_t n_items = h->rw_count;
+    while (true) {
+        if (t == 0) s_item = atomicAdd(&h->rw_counter, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        __syncthreads();
+        if (item >= n_items) break;
+        const uint2 it = rw_items[item];
+        const int tile = (int)split_list[it.x];
+        const int k = (int)it.y;
+        const uint2 rg = ranges[tile];
+        const SubTile st = sub_tile(se, tile, warp);
+        const Ray ry = make_ray<KIND>(se, st, lane);
+        const float *m = mstate + (size_t)it.x * NPART * npix + t;
+        const bool mine = __float_as_int(m[9 * npix]) == k;
+        Acc r = {m[0], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bool done = !mine, stopped = false;
+        uint32_t ne = 0, nc = 0;
+        const uint32_t s = rg.x + (uint32_t)k * L, e = min(rg.y, s + L);
+        walk<KIND, false>(rec, values, s, e, smem, st, ry, se, op, r, done, stopped, ne, nc);
+        if (mine) {
+            Acc a = {r.T, m[1 * npix] + r.A, m[2 * npix] + r.c0, m[3 * npix] + r.c1, m[4 * npix] + r.c2,
+                     m[5 * npix] + r.d, m[6 * npix] + r.n0, m[7 * npix] + r.n1, m[8 * npix] + r.n2};
+            write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
+        }
     }
 }
 
 // ---------------------------------------------------------------- host
-size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len) {
-    return RenderWs(cap, ntiles, split_len).total;
+size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix) {
+    return RenderWs(cap, ntiles, split_len, npix).total;
 }
 
 template <int KIND, bool STATS>
@@ -505,52 +597,65 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const ProjLayout PL(n, se.kind);
     const float4 *rec = (const float4 *)((const char *)proj + PL.rec);
     const int ntiles = se.ntx * se.nty;
+    const int npix = se.tw * se.th;
     // capacity implied by the workspace size (the pair capacity of gs_bin_sort)
     int64_t cap = 0;
     {
         int64_t lo = 0, hi = (int64_t)1 << 31;
         while (lo < hi) {   // largest cap whose layout fits
             const int64_t mid = (lo + hi + 1) / 2;
-            if (RenderWs(mid, ntiles, split_len).total <= ws_bytes) lo = mid; else hi = mid - 1;
+            if (RenderWs(mid, ntiles, split_len, npix).total <= ws_bytes) lo = mid; else hi = mid - 1;
         }
         cap = lo;
     }
-    const RenderWs W(cap, ntiles, split_len);
+    const RenderWs W(cap, ntiles, split_len, npix);
     char *wb = (char *)ws;
     SchedHdr *h = (SchedHdr *)(wb + W.hdr);
     uint2 *items = (uint2 *)(wb + W.items);
     uint32_t *split_base = (uint32_t *)(wb + W.split_base), *split_list = (uint32_t *)(wb + W.split_list);
     float *partials = (float *)(wb + W.partials);
-    const uint32_t L = STATS ? 0x7fffffffu : W.L;   // instrumented runs are never split
+    // instrumented runs are never split; split_len > 0 fixes the segment length
+    const uint32_t lfix = STATS ? 0x7fffffffu : (split_len > 0 ? (uint32_t)split_len : 0u);
     cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
     if (e != cudaSuccess) return e;
-    const unsigned gt = (unsigned)((ntiles + 255) / 256);
-    note_launch(3);
-    k_sched_count<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, L);
-    k_sched_scan<<<1, 32, 0, st>>>(h);
-    k_sched_fill<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, items, split_base, split_list, L);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
     constexpr int R4 = Rec<KIND>::F / 4;
-    const size_t sm = (size_t)WARPS * 2 * 32 * R4 * 16;
+    const size_t sm = (size_t)2 * npix * R4 * 16;
     e = cudaFuncSetAttribute(k_render<KIND, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, WARPS * 32, sm);
-    const unsigned grid = (unsigned)std::max(1, std::min(nsm * std::max(per, 1), (ntiles + WARPS - 1) / WARPS + nsm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, npix, sm);
+    const unsigned ctas = (unsigned)std::max(1, nsm * std::max(per, 1));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)W.max_items));
+    const unsigned gt = (unsigned)((ntiles + 255) / 256);
+    note_launch(4);
+    k_sched_total<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h);
+    k_sched_count<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, lfix, ctas);
+    k_sched_scan<<<1, 32, 0, st>>>(h);
+    k_sched_fill<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, items, split_base, split_list,
+                                     lfix, ctas);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     note_launch();
-    k_render<KIND, STATS><<<grid, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
-                                                        items, split_base, partials, o0, o1, o2, o3, stats, L);
+    k_render<KIND, STATS><<<grid, npix, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
+                                                  items, split_base, partials, o0, o1, o2, o3, stats, lfix, ctas);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!STATS && W.max_split > 0) {
-        e = cudaFuncSetAttribute(k_merge<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        float *mstate = (float *)(wb + W.mstate);
+        uint2 *rw_items = (uint2 *)(wb + W.rw_items);
+        note_launch(2);
+        k_merge_plan<KIND><<<W.max_split, npix, 0, st>>>((const uint2 *)ranges, se, op, h, split_base, split_list,
+                                                         partials, mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
+        e = cudaFuncSetAttribute(k_rewalk<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
-        note_launch();
-        k_merge<KIND><<<W.max_split, WARPS * 32, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_base,
-                                                           split_list, partials, o0, o1, o2, o3, L);
+        int per_rw = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_rw, k_rewalk<KIND>, npix, sm);
+        const unsigned grid_rw = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)nsm * std::max(per_rw, 1), (int64_t)W.max_slots));
+        k_rewalk<KIND><<<grid_rw, npix, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_list,
+                                                  mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
         e = cudaGetLastError();
     }
     return e;

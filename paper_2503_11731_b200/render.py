@@ -38,7 +38,7 @@ class Renderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda",
                  lidar_tile=(32, 1)):
         """opts apply to every frame; LiDAR frames use `lidar_tile` (columns x
-        beams of one warp-tile) unless it is None."""
+        beams of one binning tile) unless it is None."""
         self.device = torch.device(device)
         self.t = surfels
         self.n = int(surfels["means"].shape[0])
@@ -62,7 +62,11 @@ class Renderer:
     def _i32(self, name, count):
         return self._get(name, 4 * max(count, 1))[: 4 * max(count, 1)].view(torch.int32)
 
+    def opts_for(self, sensor) -> gsr.gs_opts:
+        return self.lidar_opts if sensor.kind == gsr.GS_LIDAR_SPINNING else self.cam_opts
+
     def project(self, sensor: gsr.Sensor, stream=None):
+        self.opts = self.opts_for(sensor)
         st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         proj = self._get("proj", gsr.gs_projected_bytes(self.n, sensor.kind))
         d_np = self._get("np", 8)[:8].view(torch.int64)
@@ -81,7 +85,7 @@ class Renderer:
         a buffer owned by the renderer)."""
         if not isinstance(sensor, gsr.Sensor):
             sensor = gsr.Sensor(sensor)
-        self.opts = self.lidar_opts if sensor.kind == gsr.GS_LIDAR_SPINNING else self.cam_opts
+        self.opts = self.opts_for(sensor)
         torch_stream = torch.cuda.current_stream(self.device)
         st = stream if stream is not None else torch_stream.cuda_stream
         if events is not None:

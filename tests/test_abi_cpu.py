@@ -39,7 +39,7 @@ def test_library_is_sm100a_cubin():
 
 def test_default_opts_are_north_star(gsr):
     o = gsr.default_opts()
-    assert (o.tile_w, o.tile_h) == (8, 4) and o.split_len == 0
+    assert (o.tile_w, o.tile_h) == (16, 8) and o.split_len == 0
     assert o.alpha_max == pytest.approx(0.99) and o.alpha_min == pytest.approx(1 / 255)
     assert o.t_min == pytest.approx(1e-4) and o.support_rho == 9.0
     assert o.lowpass_sigma_px == pytest.approx(2 ** -0.5) and o.near_plane == pytest.approx(0.2)
@@ -89,7 +89,7 @@ def test_host_validation_errors(gsr):
 def test_sizes(gsr):
     cam = gsr.Sensor(sg.mid(n=10).sensors[0])
     o = gsr.default_opts()
-    assert gsr.gs_num_tiles(cam, o) == 240 * 270
+    assert gsr.gs_num_tiles(cam, o) == 120 * 135
     assert gsr.gs_render_workspace_bytes(10_000_000, cam, o) > gsr.gs_render_workspace_bytes(0, cam, o)
     assert gsr.gs_record_bytes(0) == 96 and gsr.gs_record_bytes(1) == 144 and gsr.gs_record_bytes(2) == 96
     offs = gsr.gs_projected_offsets(1000, 0)

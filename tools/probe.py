@@ -19,7 +19,7 @@ from paper_2503_11731_b200.render import Renderer, to_device  # noqa: E402
 
 
 def probe(name, surfels, sensors, reps=5, opts=None, label=None):
-    ct = [int(x) for x in os.environ.get("GSR_TILE", "8,4").split(",")]
+    ct = [int(x) for x in os.environ.get("GSR_TILE", "16,8").split(",")]
     lt = [int(x) for x in os.environ.get("GSR_LTILE", "32,1").split(",")]
     r = Renderer(to_device(surfels), opts or gsr.default_opts(tile_w=ct[0], tile_h=ct[1]), lidar_tile=lt)
     res = []

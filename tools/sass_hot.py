@@ -1,0 +1,16 @@
+"""Hottest SASS instructions of a kernel in an ncu report (dev tool).
+python tools/sass_hot.py <rep> [min_frac]"""
+import csv, io, subprocess, sys
+rep = sys.argv[1]
+mn = float(sys.argv[2]) if len(sys.argv) > 2 else 0.002
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+lines = out.splitlines()
+r = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
+h = r[0]
+ie = h.index("Instructions Executed"); src = h.index("Source"); st = h.index("Warp Stall Sampling (All Samples)")
+rows = [(x[0], x[src], int(x[ie] or 0), int(x[st] or 0)) for x in r[1:] if len(x) > ie]
+tot = sum(x[2] for x in rows); tst = sum(x[3] for x in rows)
+print("total inst", tot, "samples", tst)
+for a, s, n, smp in rows:
+    if n >= mn * tot or smp >= 0.01 * tst:
+        print(f"{a[-5:]} {n / tot * 100:5.1f}% {smp / max(tst,1) * 100:5.1f}%st {s.strip()}")
