@@ -160,7 +160,10 @@ static DevSensor make_dev_sensor(const gs_sensor *s, const gs_opts *o) {
     d.az_step = s->azimuth_step;
     if (s->kind == GS_LIDAR_SPINNING) {
         d.nbeams = s->height;
-        for (int r = 0; r < s->height; ++r) d.beam[r] = s->beam_elevation[r];
+        for (int r = 0; r < s->height; ++r) {
+            d.beam[r] = s->beam_elevation[r];
+            d.sbeam[r] = (float)sin((double)s->beam_elevation[r]);
+        }
         d.full_turn = fabs((double)s->width * (double)s->azimuth_step - 2.0 * M_PI) < 1e-5;
     }
     return d;

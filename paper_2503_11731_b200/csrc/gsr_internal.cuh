@@ -24,6 +24,7 @@ struct DevSensor {
     int32_t nbeams;
     int32_t full_turn;          // LiDAR: width*az_step covers 2pi (azimuth wraps)
     float beam[GS_MAX_BEAMS];
+    float sbeam[GS_MAX_BEAMS];  // sin(beam), fp64-evaluated, rounded to fp32
 };
 
 struct DevOpts {

@@ -175,20 +175,20 @@ __device__ __forceinline__ double dot3(const double a[3], const double b[3]) {
     return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
 }
 
-// LiDAR: rows whose beam elevation lies in [lo, hi] (table strictly decreasing)
+// LiDAR: rows whose beam elevation sine lies in [lo, hi] (table strictly decreasing)
 __device__ __forceinline__ bool beam_rows(const DevSensor &se, double lo, double hi, int &r0, int &r1) {
-    // first row with beam <= hi
+    // first row with sin(beam) <= hi
     int a = 0, b = se.nbeams;
     while (a < b) {
         const int m = (a + b) >> 1;
-        if ((double)se.beam[m] <= hi) b = m; else a = m + 1;
+        if ((double)se.sbeam[m] <= hi) b = m; else a = m + 1;
     }
     r0 = a;
-    // last row with beam >= lo
+    // last row with sin(beam) >= lo
     a = 0; b = se.nbeams;
     while (a < b) {
         const int m = (a + b) >> 1;
-        if ((double)se.beam[m] < lo) b = m; else a = m + 1;
+        if ((double)se.sbeam[m] < lo) b = m; else a = m + 1;
     }
     r1 = a - 1;
     return r0 <= r1;
@@ -199,6 +199,7 @@ __device__ __forceinline__ bool beam_rows(const DevSensor &se, double lo, double
 // azc + [daz_lo, daz_hi] unless all_az.
 struct AngBox {
     double el_lo, el_hi, azc, daz_lo, daz_hi;
+    double s_lo, s_hi;      // sines of el_lo, el_hi (LiDAR rows are found by sine, no asin)
     bool all_az;
 };
 
@@ -234,7 +235,8 @@ __device__ void lf_range(double n0, double n1, double n2, double d0, double d1, 
 // in (c,s); the direction m + xi e_az + eta e_el then bounds elevation and
 // azimuth with numerator/denominator interval arithmetic.  Returns false if
 // the disk reaches the plane P.m = 0 or the centre is at the pole.
-__device__ bool angular_box_disk(const double mu[3], const double a[3], const double b[3], AngBox &ab) {
+__device__ bool angular_box_disk(const double mu[3], const double a[3], const double b[3], AngBox &ab,
+                                 bool need_el) {
     const double r = sqrt(dot3(mu, mu));
     const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
     const double rho = sqrt(m[0] * m[0] + m[1] * m[1]);
@@ -255,16 +257,20 @@ __device__ bool angular_box_disk(const double mu[3], const double a[3], const do
     const double nlo = m[2] + yl * rho, nhi = m[2] + yh * rho;
     const double shi = nhi > 0.0 ? nhi / den_lo : nhi / den_hi;
     const double slo = nlo > 0.0 ? nlo / den_hi : nlo / den_lo;
-    ab.el_hi = asin(fmin(1.0, shi)) + 1e-7;
-    ab.el_lo = asin(fmax(-1.0, slo)) - 1e-7;
-    // azimuth: tan(daz) = xi / (rho - eta*m_z)
+    ab.s_hi = fmin(1.0, shi) + 1e-9;
+    ab.s_lo = fmax(-1.0, slo) - 1e-9;
+    if (need_el) {
+        ab.el_hi = asin(fmin(1.0, shi)) + 1e-7;
+        ab.el_lo = asin(fmax(-1.0, slo)) - 1e-7;
+    }
+    // azimuth: tan(daz) = xi / (rho - eta*m_z); fp32 arctangents, 5e-6 rad margin
     const double t1 = yl * m[2], t2 = yh * m[2];
     const double Dlo = rho - fmax(t1, t2), Dhi = rho - fmin(t1, t2);
-    ab.azc = atan2(m[1], m[0]);
-    ab.all_az = !(Dlo > 1e-9) || ab.el_hi >= 0.5 * M_PI || ab.el_lo <= -0.5 * M_PI;
+    ab.azc = (double)atan2f((float)m[1], (float)m[0]);
+    ab.all_az = !(Dlo > 1e-9) || ab.s_hi >= 1.0 || ab.s_lo <= -1.0;
     if (!ab.all_az) {
-        ab.daz_hi = atan(xh > 0.0 ? xh / Dlo : xh / Dhi) + 1e-7;
-        ab.daz_lo = atan(xl < 0.0 ? xl / Dlo : xl / Dhi) - 1e-7;
+        ab.daz_hi = (double)atanf((float)(xh > 0.0 ? xh / Dlo : xh / Dhi)) + 5e-6;
+        ab.daz_lo = (double)atanf((float)(xl < 0.0 ? xl / Dlo : xl / Dhi)) - 5e-6;
     }
     return true;
 }
@@ -274,6 +280,8 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
     const double elc = asin(fmin(1.0, fmax(-1.0, m[2])));
     ab.el_lo = elc - beta;
     ab.el_hi = elc + beta;
+    ab.s_lo = ab.el_lo <= -0.5 * M_PI ? -1.0 : sin(ab.el_lo) - 1e-9;
+    ab.s_hi = ab.el_hi >= 0.5 * M_PI ? 1.0 : sin(ab.el_hi) + 1e-9;
     ab.azc = atan2(m[1], m[0]);
     ab.all_az = beta >= 0.5 * M_PI - fabs(elc);
     if (!ab.all_az) {
@@ -475,7 +483,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             if (!whole) {
                 double a[3], b[3];
                 for (int k = 0; k < 3; ++k) { a[k] = Rr * su * A[k]; b[k] = Rr * sv * Bv[k]; }
-                if (!angular_box_disk(mu, a, b, ab)) angular_box_cap(m, asin(R3 / r), ab);
+                if (!angular_box_disk(mu, a, b, ab, KIND == GS_FISHEYE_EQUIDISTANT)) angular_box_cap(m, asin(R3 / r), ab);
             }
             if (KIND == GS_FISHEYE_EQUIDISTANT) {
                 Box bx;
@@ -522,8 +530,8 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                 int r0 = 0, r1 = se.nbeams - 1, c0 = 0, c1 = W - 1;
                 bool allaz = whole;
                 if (!whole) {
-                    const double eps = 1e-6;
-                    vis = beam_rows(se, ab.el_lo - eps, ab.el_hi + eps, r0, r1);
+                    const double eps = 2e-6;   // sine units; covers the fp32 sine table
+                    vis = beam_rows(se, ab.s_lo - eps, ab.s_hi + eps, r0, r1);
                     allaz = ab.all_az;
                     if (!allaz) {
                         const double step = (double)se.az_step;

@@ -55,10 +55,13 @@ constexpr int NPART = 10;                                // floats per partial c
 constexpr uint32_t LMIN = 1024;   // shortest segment of the adaptive split (workspace sizing)
 constexpr unsigned FULL = 0xffffffffu;
 
+// F: floats per record; BB: float index of the packed pixel box; S4: record
+// stride in shared memory in 16-byte units (all lanes of a warp read the same
+// record: broadcast, no bank conflicts).
 template <int KIND> struct Rec;
-template <> struct Rec<GS_PINHOLE> { static constexpr int F = PH_FLOATS, BB = PH_BBX; };
-template <> struct Rec<GS_FISHEYE_EQUIDISTANT> { static constexpr int F = FE_FLOATS, BB = FE_BBX; };
-template <> struct Rec<GS_LIDAR_SPINNING> { static constexpr int F = LI_FLOATS, BB = LI_BBX; };
+template <> struct Rec<GS_PINHOLE> { static constexpr int F = PH_FLOATS, BB = PH_BBX, S4 = PH_FLOATS / 4; };
+template <> struct Rec<GS_FISHEYE_EQUIDISTANT> { static constexpr int F = FE_FLOATS, BB = FE_BBX, S4 = FE_FLOATS / 4; };
+template <> struct Rec<GS_LIDAR_SPINNING> { static constexpr int F = LI_FLOATS, BB = LI_BBX, S4 = LI_FLOATS / 4; };
 
 // ---------------------------------------------------------------- workspace
 struct SchedHdr {
@@ -278,7 +281,7 @@ __device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint3
                                      uint32_t s, uint32_t e, float4 *smem, const SubTile &st, const Ray &ry,
                                      const DevSensor &se, const DevOpts &op, Acc &a, bool &done, bool &stopped,
                                      uint32_t &n_eval, uint32_t &n_comp) {
-    constexpr int R4 = Rec<KIND>::F / 4;
+    constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
     const int B = blockDim.x, t = threadIdx.x, lane = t & 31;
     bool wdone = __all_sync(FULL, done);
@@ -287,7 +290,7 @@ __device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint3
         if (first + t < e) {
             const uint32_t id = __ldg(values + first + t);
             const float4 *src = rec + (size_t)id * R4;
-            float4 *d = dst + t * R4;
+            float4 *d = dst + t * S4;
 #pragma unroll
             for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
         }
@@ -297,19 +300,19 @@ __device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint3
     stage(s, smem);
     for (uint32_t b = 0; b < nb; ++b) {
         if (b + 1 < nb) {
-            stage(s + (b + 1) * B, smem + ((b + 1) & 1) * B * R4);
+            stage(s + (b + 1) * B, smem + ((b + 1) & 1) * B * S4);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const float4 *buf = smem + (b & 1) * B * R4;
+        const float4 *buf = smem + (b & 1) * B * S4;
         const int cnt = (int)min((uint32_t)B, e - (s + b * B));
         if (!wdone) {
             for (int c = 0; c < cnt; c += 32) {
                 bool hit = false;
                 if (c + lane < cnt) {
-                    const float4 bb = buf[(c + lane) * R4 + BB4];
+                    const float4 bb = buf[(c + lane) * S4 + BB4];
                     hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
                 }
                 uint32_t bits = __ballot_sync(FULL, hit);
@@ -318,7 +321,7 @@ __device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint3
                     do {
                         const int j = __ffs(bits) - 1;
                         bits &= bits - 1;
-                        if (!eval_record<KIND, STATS>(buf + (c + j) * R4, ry, op, a, n_eval, n_comp)) {
+                        if (!eval_record<KIND, STATS>(buf + (c + j) * S4, ry, op, a, n_eval, n_comp)) {
                             done = true;
                             stopped = true;
                             break;
@@ -618,8 +621,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const uint32_t lfix = STATS ? 0x7fffffffu : (split_len > 0 ? (uint32_t)split_len : 0u);
     cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
     if (e != cudaSuccess) return e;
-    constexpr int R4 = Rec<KIND>::F / 4;
-    const size_t sm = (size_t)2 * npix * R4 * 16;
+    const size_t sm = (size_t)2 * npix * Rec<KIND>::S4 * 16;
     e = cudaFuncSetAttribute(k_render<KIND, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, per = 1;
