@@ -277,29 +277,73 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_pair_offsets(
 }
 
 // ------------------------------------------------------------------ emission
-// One thread per visible surfel (depth order): its tiles, row-major, at its
-// offset.  Tile ids are reduced modulo ntx (LiDAR azimuth wrap).
+// Warp-cooperative: a warp takes 32 consecutive visible surfels (depth
+// order), whose pairs occupy one contiguous output range; lane q of each
+// round writes pair q of that range (coalesced), locating its surfel by a
+// binary search over the warp's exclusive pair counts.  Pairs of a surfel
+// are its tiles row-major (tile column modulo ntx: LiDAR azimuth wrap).
+// The per-digit histograms of the tile sort (npass x 8-bit digits) are
+// accumulated on the way in shared memory and added to `thist`.
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
                                               const uint32_t *__restrict__ offs,
                                               const short4 *__restrict__ rect,
-                                              const ProjHeader *hdr, int ntx,
+                                              const ProjHeader *hdr, int ntx, int npass, int tbits,
                                               uint32_t *__restrict__ tkey,
-                                              uint32_t *__restrict__ tval,
+                                              uint32_t *__restrict__ tval, uint32_t *__restrict__ thist,
                                               const int32_t *d_overflow) {
+    __shared__ uint32_t h[3][RS_BINS];
     if (*d_overflow) return;
+    for (int i = threadIdx.x; i < 3 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
     const uint32_t n = hdr->n_visible;
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const uint32_t id = sid[k];
-    uint32_t o = offs[k];
-    const short4 r = rect[id];
-    for (int ty = r.y; ty <= r.w; ++ty)
-        for (int tx = r.x; tx <= r.z; ++tx) {
-            const int t = tx >= ntx ? tx - ntx : tx;
-            tkey[o] = (uint32_t)(ty * ntx + t);
-            tval[o] = id;
-            ++o;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < n; w += nwarps) {
+        const uint32_t k = w * 32 + lane;
+        uint32_t id = 0, c = 0, o0 = 0;
+        int x0 = 0, y0 = 0, wd = 1;
+        if (k < n) {
+            id = sid[k];
+            const short4 r = rect[id];
+            x0 = r.x; y0 = r.y;
+            wd = r.z - r.x + 1;
+            c = (uint32_t)(wd * (r.w - r.y + 1));
+            o0 = offs[k];
         }
+        const uint32_t base = __shfl_sync(FULL_MASK, o0, 0);
+        const uint32_t inc = warp_inclusive_scan<uint32_t>(c);
+        const uint32_t lo = inc - c;
+        const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
+        for (uint32_t o = 0; o < total; o += 32) {
+            const uint32_t q = o + lane;
+            int idx = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const uint32_t l = __shfl_sync(FULL_MASK, lo, idx + step);
+                if (q >= l && idx + step < 32) idx += step;
+            }
+            const uint32_t rid = __shfl_sync(FULL_MASK, id, idx);
+            const uint32_t rlo = __shfl_sync(FULL_MASK, lo, idx);
+            const int rx0 = __shfl_sync(FULL_MASK, x0, idx), ry0 = __shfl_sync(FULL_MASK, y0, idx);
+            const int rw = __shfl_sync(FULL_MASK, wd, idx);
+            if (q < total) {
+                const uint32_t r = q - rlo;
+                const int dy = (int)(r / (uint32_t)rw), dx = (int)(r - (uint32_t)dy * (uint32_t)rw);
+                const int tx = rx0 + dx;
+                const uint32_t tile = (uint32_t)((ry0 + dy) * ntx + (tx >= ntx ? tx - ntx : tx));
+                tkey[base + q] = tile;
+                tval[base + q] = rid;
+                for (int p = 0; p < npass; ++p) {
+                    const int bits = min(8, tbits - 8 * p);
+                    atomicAdd(&h[p][(tile >> (8 * p)) & ((1u << bits) - 1)], 1u);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; ++p)
+        for (int b = threadIdx.x; b < RS_BINS; b += blockDim.x)
+            if (h[p][b]) atomicAdd(&thist[p * RS_BINS + b], h[p][b]);
 }
 
 // ------------------------------------------------------------------ ranges
@@ -397,17 +441,18 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     uint32_t *tv[2] = {values, (uint32_t *)(wb + W.tv1)};
     int cur = np & 1;
     note_launch();
-    k_emit<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr,
-                                                         ntx, tk[cur], tv[cur], d_overflow);
-    CK(cudaGetLastError());
-    // 3. tile digits over the pairs
+    // emission fused with the tile-digit histograms
     const int tb = tile_bits_for(ntiles);
     const uint32_t *d_np = &misc->n_pairs32;
     uint32_t *thist = hist + 4 * RS_BINS;
-    const unsigned hgrid_t = (unsigned)std::min<int64_t>((cap + 4095) / 4096, 4 * 148);
-    note_launch();
-    k_hist<<<hgrid_t > 0 ? hgrid_t : 1, 256, 0, st>>>(tk[cur], d_np, np, tb, thist, d_overflow);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)nsm * 8));
+    k_emit<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr, ntx, np, tb, tk[cur], tv[cur],
+                               thist, d_overflow);
     CK(cudaGetLastError());
+    // 3. tile digits over the pairs
     note_launch();
     k_hist_scan<<<1, RS_BINS, 0, st>>>(thist, np, d_overflow);
     CK(cudaGetLastError());
