@@ -67,8 +67,8 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
         const double Y = mu[1] + c * a[1] + s * b[1];
         const double Z = mu[2] + c * a[2] + s * b[2];
         if (Z >= nearp * (1.0 - 1e-9)) {
-            const double zz = fmax(Z, nearp * (1.0 - 1e-9));
-            box.add((double)se.fx * X / zz + (double)se.cx, (double)se.fy * Y / zz + (double)se.cy);
+            const double iz = 1.0 / fmax(Z, nearp * (1.0 - 1e-9));
+            box.add((double)se.fx * X * iz + (double)se.cx, (double)se.fy * Y * iz + (double)se.cy);
         }
     };
     auto solve = [&](double A, double B, double C, bool strict) {
@@ -77,8 +77,9 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
         double disc = rr - C * C;
         if (strict && !(disc > 0.0)) return;
         disc = sqrt(fmax(disc, 0.0));
-        add_pt((-A * C + B * disc) / rr, (-B * C - A * disc) / rr);
-        add_pt((-A * C - B * disc) / rr, (-B * C + A * disc) / rr);
+        const double irr = 1.0 / rr;
+        add_pt((-A * C + B * disc) * irr, (-B * C - A * disc) * irr);
+        add_pt((-A * C - B * disc) * irr, (-B * C + A * disc) * irr);
     };
     add_pt(0.0, 0.0);
     add_pt(1.0, 0.0);
@@ -416,6 +417,11 @@ template <int KIND>
 __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op,
                                             int64_t i, float *__restrict__ rec, short4 *__restrict__ rect,
                                             uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
+    if (KIND != GS_LIDAR_SPINNING && s.sh) {   // the SH block is read last: start it towards L2 now
+        const int nc3 = (s.sh_degree + 1) * (s.sh_degree + 1) * 3;
+        const char *p = reinterpret_cast<const char *>(s.sh + (size_t)i * nc3);
+        for (int b = 0; b < nc3 * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+    }
     const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1),
                 mz = __ldg(s.means + 3 * i + 2);
     double mu[3];
@@ -444,8 +450,8 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
     if (vis) {
         const float4 qf = __ldg(reinterpret_cast<const float4 *>(s.quats) + i);
         double qw = qf.x, qx = qf.y, qy = qf.z, qz = qf.w;
-        const double nq = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-        qw /= nq; qx /= nq; qy /= nq; qz /= nq;
+        const double inq = rsqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+        qw *= inq; qx *= inq; qy *= inq; qz *= inq;
         const double Rq[3][3] = {
             {1.0 - 2.0 * (qy * qy + qz * qz), 2.0 * (qx * qy - qw * qz), 2.0 * (qx * qz + qw * qy)},
             {2.0 * (qx * qy + qw * qz), 1.0 - 2.0 * (qx * qx + qz * qz), 2.0 * (qy * qz - qw * qx)},
@@ -608,9 +614,9 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         R[PH_A20] = (float)(N[0] * ifx);
         R[PH_A21] = (float)(N[1] * ify);
         R[PH_QC] = (float)(det / mu[2]);
-        R[PH_RCUT3] = rcut3;
         const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
         const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
+        R[PH_RCUT3] = rcut3;
         split_hilo(cx, R[PH_CHX], R[PH_CLX]);
         split_hilo(cy, R[PH_CHY], R[PH_CLY]);
         R[PH_RCUT2] = rcut3 * op.sigma2;
@@ -683,7 +689,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
 
 // One thread per candidate (grid-stride over the compacted list of k_cull).
 template <int KIND>
-__global__ void __launch_bounds__(256, 2) k_project(DevSurfels s, const __grid_constant__ DevSensor se, DevOpts op,
+__global__ void __launch_bounds__(256, 3) k_project(DevSurfels s, const __grid_constant__ DevSensor se, DevOpts op,
                                                  const uint32_t *__restrict__ cand, const ProjHeader *hdr,
                                                  float *__restrict__ rec, short4 *__restrict__ rect,
                                                  uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {

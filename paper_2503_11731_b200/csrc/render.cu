@@ -6,13 +6,15 @@
 // o G), skip alpha < alpha_min, stop before T < t_min.
 //
 // Work decomposition (B200): one CTA composites one binning
-// tile (opts tile_w x tile_h samples); each of its warps owns a 32-sample
-// sub-tile (8x4 pixels for cameras, 32x1 LiDAR columns of one beam).  The CTA
-// stages its tile's depth-sorted surfel records into shared memory with
-// cp.async, one record per thread per batch (double buffered), so every
-// record is fetched from L2/HBM once per tile; each warp then ballots which
-// records of the batch touch its sub-tile (conservative pixel box) and walks
-// only those, in list order, with warp-vote early termination.  CTAs are
+// tile (opts tile_w x tile_h samples); each of its consumer warps owns a
+// 32-sample sub-tile (8x4 pixels for cameras, 32x1 LiDAR columns of one beam)
+// and one producer warp streams the tile's depth-sorted surfel records into a
+// shared-memory ring with TMA bulk copies completing on mbarriers, so every
+// record is fetched from L2/HBM once per tile and the consumer warps drift up
+// to a ring's length apart instead of meeting at a barrier per batch.  Each
+// consumer ballots which records of a slot touch its sub-tile (conservative
+// pixel box) and walks only those, in list order, with warp-vote early
+// termination; the producer stops when all consumers are done.  CTAs are
 // persistent and pull work items (tile, segment) from a longest-first
 // schedule built on the device.  Lists longer than split_len are cut into
 // segments composited in parallel; a merge kernel combines the segment
@@ -205,23 +207,25 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
         const float4 bb = r[BB4];
         if (in_box(__float_as_uint(bb.z), __float_as_uint(bb.w), ry.pxi, ry.pxw, ry.pyi)) ++n_eval;
     }
-    float rho3, rho2, ir, dep3, depc, o;
+    float rho, dep, o;
     if (KIND == GS_PINHOLE) {
         const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3];
         const float dx = (ry.px - g2.x) - g2.z, dy = (ry.py - g2.y) - g2.w;
+        const float s2 = fmaf(dx, dx, dy * dy);
         const float q0 = fmaf(g0.x, dx, g0.y * dy);
         const float q1 = fmaf(g0.z, dx, g0.w * dy);
         const float q2 = fmaf(g1.x, dx, fmaf(g1.y, dy, g1.z));
         const float n3 = fmaf(q0, q0, q1 * q1);
-        const float s2 = fmaf(dx, dx, dy * dy);
         if ((n3 > g1.w * q2 * q2) && (s2 > g3.x)) return true;
-        ir = fast_rcp(q2);
-        rho3 = n3 * ir * ir;
-        rho2 = s2 * op.inv_sigma2;
-        dep3 = g3.z * ir;
-        depc = g3.w;
+        const float ir = fast_rcp(q2);
+        const float rho3 = n3 * ir * ir;
+        const float rho2 = s2 * op.inv_sigma2;
+        const bool use3 = rho3 <= rho2;
+        rho = use3 ? rho3 : rho2;
+        dep = use3 ? g3.z * ir : g3.w;
         o = g3.y;
     } else {
+        float rho3, rho2, ir, dep3, depc;
         const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3], g4 = r[4];
         const float ex = (ry.dh[0] - g0.x) + (ry.dl[0] - g1.x);
         const float ey = (ry.dh[1] - g0.y) + (ry.dl[1] - g1.y);
@@ -245,10 +249,10 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
         dep3 = g3.w * ir;
         depc = g4.w;
         o = g2.w;
+        const bool use3 = rho3 <= rho2;
+        rho = use3 ? rho3 : rho2;
+        dep = use3 ? dep3 : depc;
     }
-    const bool use3 = rho3 <= rho2;
-    const float rho = use3 ? rho3 : rho2;
-    const float dep = use3 ? dep3 : depc;
     if (!(rho <= op.support) || !(dep >= op.near_plane)) return true;
     const float al = fminf(op.alpha_max, o * fast_ex2(-LOG2E_HALF * rho));
     if (!(al >= op.alpha_min)) return true;
@@ -272,70 +276,214 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
     return true;
 }
 
+// ---------------------------------------------------------------- staging pipeline
+// Warp-specialised: the last warp of the CTA is the producer -- it copies the
+// depth-sorted records of the tile list into a ring of KSLOTS slots (32
+// records each, one record per lane as 16-byte cp.async ops whose completion
+// arrives on the slot's `full` mbarrier; measured faster than one TMA bulk
+// copy per 96-byte record, which are too small to amortise); the other warps are
+// consumers, one per 32-sample sub-tile, and release a slot on its `empty`
+// mbarrier.  Consumers run up to KSLOTS batches apart instead of meeting at a
+// CTA barrier per batch.  When every consumer's samples have stopped, the
+// producer publishes a STOP slot instead of more records.
+constexpr int KSLOTS = 8;
+struct Pipe {
+    unsigned long long full[KSLOTS], empty[KSLOTS];
+    uint32_t stop_seq[KSLOTS];   // batch clock of a STOP slot
+    int n_done;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(void *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(void *b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, void *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async_arrive(void *b) {   // arrive when this thread's cp.async ops land
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void pipe_init(Pipe &pp, int nw) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < KSLOTS; ++k) {
+            mbar_init(&pp.full[k], 32);   // the 32 producer lanes
+            mbar_init(&pp.empty[k], (uint32_t)nw);
+            pp.stop_seq[k] = 0xffffffffu;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
 // CTA walk of list entries [s, e) of `values`; every thread of the CTA calls
-// it (it holds barriers).  smem: 2 x blockDim records.  Each thread's sample
-// is `ry` in its warp's sub-tile `st`; `done` lanes skip work and a lane
-// becomes done when its ray stops (`stopped`).
+// it.  Consumer thread: its sample `ry` in its warp's sub-tile `st`; `done`
+// lanes skip work and a lane becomes done when its ray stops (`stopped`).
+// g: batches used so far by this CTA (the ring's phase clock, equal in all
+// threads).
 template <int KIND, bool STATS>
-__device__ __forceinline__ void walk(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
-                                     uint32_t s, uint32_t e, float4 *smem, const SubTile &st, const Ray &ry,
-                                     const DevSensor &se, const DevOpts &op, Acc &a, bool &done, bool &stopped,
-                                     uint32_t &n_eval, uint32_t &n_comp) {
+__device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+                                     uint32_t s, uint32_t e, float4 *ring, Pipe &pp, uint32_t &g,
+                                     const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
+                                     Acc &a, bool &done, bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
-    const int B = blockDim.x, t = threadIdx.x, lane = t & 31;
-    bool wdone = __all_sync(FULL, done);
-    if (__syncthreads_count(!wdone) == 0 || s >= e) return;
-    auto stage = [&](uint32_t first, float4 *dst) {
-        if (first + t < e) {
-            const uint32_t id = __ldg(values + first + t);
-            const float4 *src = rec + (size_t)id * R4;
-            float4 *d = dst + t * S4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5) - 1;
+    const uint32_t nb = s < e ? (e - s + 31) >> 5 : 0u;
+    if (threadIdx.x == 0) pp.n_done = 0;
+    __syncthreads();
+    bool wdone = true;
+    if (warp < nw) {
+        wdone = __all_sync(FULL, done);
+        if (wdone && lane == 0) atomicAdd(&pp.n_done, 1);
+    }
+    __syncthreads();
+    uint32_t used = nb;
+    if (warp == nw) {   // producer
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint32_t gg = g + b, slot = gg % KSLOTS;
+            if (gg >= KSLOTS) mbar_wait(&pp.empty[slot], ((gg / KSLOTS) & 1u) ^ 1u);
+            // one read, broadcast: the lanes must agree on STOP
+            const bool stop = __shfl_sync(FULL, *(volatile int *)&pp.n_done, 0) >= nw;
+            if (stop) {
+                if (lane == 0) pp.stop_seq[slot] = gg;
+                __syncwarp();
+                mbar_arrive(&pp.full[slot]);   // release: the STOP mark is visible to the waiters
+                used = b + 1;
+                break;
+            }
+            const uint32_t first = s + b * 32;
+            if (first + lane < e) {
+                const uint32_t id = __ldg(values + first + lane);
+                const float4 *src = rec + (size_t)id * R4;
+                float4 *dst = ring + (slot * 32 + lane) * S4;
 #pragma unroll
-            for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
+                for (int k = 0; k < R4; ++k) cp_async16(dst + k, src + k);
+            }
+            cp_async_arrive(&pp.full[slot]);
         }
-        cp_async_commit();
-    };
-    const uint32_t nb = (e - s + B - 1) / B;
-    stage(s, smem);
-    for (uint32_t b = 0; b < nb; ++b) {
-        if (b + 1 < nb) {
-            stage(s + (b + 1) * B, smem + ((b + 1) & 1) * B * S4);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const float4 *buf = smem + (b & 1) * B * S4;
-        const int cnt = (int)min((uint32_t)B, e - (s + b * B));
-        if (!wdone) {
-            for (int c = 0; c < cnt; c += 32) {
+    } else {   // consumers
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint32_t gg = g + b, slot = gg % KSLOTS;
+            mbar_wait(&pp.full[slot], (gg / KSLOTS) & 1u);
+            const int cnt = *(volatile uint32_t *)&pp.stop_seq[slot] == gg ? -1 : (int)min(32u, e - (s + b * 32));
+            if (cnt >= 0 && !wdone) {
+                const float4 *buf = ring + slot * 32 * S4;
                 bool hit = false;
-                if (c + lane < cnt) {
-                    const float4 bb = buf[(c + lane) * S4 + BB4];
+                if (lane < cnt) {
+                    const float4 bb = buf[lane * S4 + BB4];
                     hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
                 }
                 uint32_t bits = __ballot_sync(FULL, hit);
-                if (!bits) continue;
-                if (!done) {
+                if (bits && !done) {
                     do {
                         const int j = __ffs(bits) - 1;
                         bits &= bits - 1;
-                        if (!eval_record<KIND, STATS>(buf + (c + j) * S4, ry, op, a, n_eval, n_comp)) {
+                        if (!eval_record<KIND, STATS>(buf + j * S4, ry, op, a, n_eval, n_comp)) {
                             done = true;
                             stopped = true;
                             break;
                         }
                     } while (bits);
                 }
-                if (__all_sync(FULL, done)) { wdone = true; break; }
+                if (__all_sync(FULL, done)) {
+                    wdone = true;
+                    if (lane == 0) atomicAdd(&pp.n_done, 1);
+                }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pp.empty[slot]);
+            if (cnt < 0) { used = b + 1; break; }
         }
-        // every warp is past batch b (its buffer may be restaged); stop once all warps are done
-        if (__syncthreads_count(!wdone) == 0) break;
+    }
+    g += used;
+    __syncthreads();
+}
+
+// One-warp tiles (LiDAR 32x1): no producer warp -- the warp stages its own
+// list into a double buffer of 2 x 32 records with cp.async and walks it.
+template <int KIND, bool STATS>
+__device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+                                          uint32_t s, uint32_t e, float4 *buf2, const SubTile &st, const Ray &ry,
+                                          const DevSensor &se, const DevOpts &op, Acc &a, bool &done,
+                                          bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
+    constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
+    constexpr int BB4 = Rec<KIND>::BB / 4;
+    const int lane = threadIdx.x & 31;
+    if (__all_sync(FULL, done) || s >= e) return;
+    auto stage = [&](uint32_t first, float4 *dst) {
+        if (first + lane < e) {
+            const uint32_t id = __ldg(values + first + lane);
+            const float4 *src = rec + (size_t)id * R4;
+            float4 *d = dst + lane * S4;
+#pragma unroll
+            for (int k = 0; k < R4; ++k) cp_async16(d + k, src + k);
+        }
+        cp_async_commit();
+    };
+    const uint32_t nb = (e - s + 31) >> 5;
+    stage(s, buf2);
+    for (uint32_t b = 0; b < nb; ++b) {
+        if (b + 1 < nb) {
+            stage(s + (b + 1) * 32, buf2 + ((b + 1) & 1) * 32 * S4);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const float4 *buf = buf2 + (b & 1) * 32 * S4;
+        const int cnt = (int)min(32u, e - (s + b * 32));
+        bool hit = false;
+        if (lane < cnt) {
+            const float4 bb = buf[lane * S4 + BB4];
+            hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
+        }
+        uint32_t bits = __ballot_sync(FULL, hit);
+        if (bits && !done) {
+            do {
+                const int j = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (!eval_record<KIND, STATS>(buf + j * S4, ry, op, a, n_eval, n_comp)) {
+                    done = true;
+                    stopped = true;
+                    break;
+                }
+            } while (bits);
+        }
+        if (__all_sync(FULL, done)) break;
+        __syncwarp();
     }
     cp_async_wait<0>();
-    __syncthreads();
+    __syncwarp();
+}
+
+template <int KIND, bool STATS>
+__device__ __forceinline__ void walk(bool piped, const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+                                     uint32_t s, uint32_t e, float4 *smem, Pipe &pp, uint32_t &g,
+                                     const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
+                                     Acc &a, bool &done, bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
+    if (piped)
+        walk_pipe<KIND, STATS>(rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+    else
+        walk_self<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, n_eval, n_comp);
 }
 
 template <int KIND>
@@ -375,12 +523,14 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t len, uint32_t L) {
     return b >= NB ? NB - 1 : b;
 }
 
-// Segment length: fixed (opts split_len > 0), else adaptive -- about half a
-// fair share of the frame's pairs per resident CTA (at least LMIN), so the
-// longest-first schedule keeps every SM busy to the end.
+// Segment length: fixed (opts split_len > 0), else adaptive -- an eighth of
+// a fair share of the frame's pairs per resident CTA (at least LMIN), so the
+// longest-first schedule keeps every SM busy to the end and the exact-stop
+// re-walk of one segment stays short (measured best on the Chunked forward
+// camera, tools/sweep.py).
 __device__ __forceinline__ uint32_t seg_len(const SchedHdr *h, uint32_t lfix, uint32_t ctas) {
     if (lfix) return lfix;
-    const uint32_t share = (h->P / (2u * ctas) + 255u) & ~255u;
+    const uint32_t share = (h->P / (8u * ctas) + 255u) & ~255u;
     return share > LMIN ? share : LMIN;
 }
 
@@ -439,7 +589,7 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 // segment).  Unsplit tiles are written out; segments of split tiles leave
 // their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
-__global__ void __launch_bounds__(512) k_render(
+__global__ void __launch_bounds__(544) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
@@ -449,9 +599,15 @@ __global__ void __launch_bounds__(512) k_render(
     const uint32_t L = seg_len(h, lfix, ctas);
     extern __shared__ float4 smem[];
     __shared__ uint32_t s_item;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
+    __shared__ Pipe pp;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const bool piped = blockDim.x > 32;   // one-warp tiles stage for themselves
+    const int nw = piped ? (int)(blockDim.x >> 5) - 1 : 1, npix = nw * 32;
+    const bool cons = warp < nw;
     const bool ovf = d_overflow && *d_overflow;
     const uint32_t n_items = h->n_items;
+    if (piped) pipe_init(pp, nw);
+    uint32_t g = 0;
     while (true) {
         if (t == 0) s_item = atomicAdd(&h->counter, 1u);
         __syncthreads();
@@ -470,7 +626,8 @@ __global__ void __launch_bounds__(512) k_render(
         Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !ry.valid, stopped = false;
         uint32_t n_eval = 0, n_comp = 0;
-        walk<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+        walk<KIND, STATS>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+        if (!cons) continue;
         if (ns == 1) {
             write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
             if (STATS && ry.inside) {
@@ -549,7 +706,7 @@ __global__ void __launch_bounds__(512) k_merge_plan(
 // from each stopping sample's prefix transmittance; the segment's result is
 // added to the prefix composite and the sample written out.
 template <int KIND>
-__global__ void __launch_bounds__(512) k_rewalk(
+__global__ void __launch_bounds__(544) k_rewalk(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
     SchedHdr *h, const uint32_t *__restrict__ split_list, const float *__restrict__ mstate,
@@ -558,8 +715,14 @@ __global__ void __launch_bounds__(512) k_rewalk(
     const uint32_t L = seg_len(h, lfix, ctas);
     extern __shared__ float4 smem[];
     __shared__ uint32_t s_item;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
+    __shared__ Pipe pp;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const bool piped = blockDim.x > 32;
+    const int nw = piped ? (int)(blockDim.x >> 5) - 1 : 1, npix = nw * 32;
+    const bool cons = warp < nw;
     const uint32_t n_items = h->rw_count;
+    if (piped) pipe_init(pp, nw);
+    uint32_t g = 0;
     while (true) {
         if (t == 0) s_item = atomicAdd(&h->rw_counter, 1u);
         __syncthreads();
@@ -572,13 +735,13 @@ __global__ void __launch_bounds__(512) k_rewalk(
         const uint2 rg = ranges[tile];
         const SubTile st = sub_tile(se, tile, warp);
         const Ray ry = make_ray<KIND>(se, st, lane);
-        const float *m = mstate + (size_t)it.x * NPART * npix + t;
-        const bool mine = __float_as_int(m[9 * npix]) == k;
+        const float *m = mstate + (size_t)it.x * NPART * npix + (cons ? t : 0);
+        const bool mine = cons && __float_as_int(m[9 * npix]) == k;
         Acc r = {m[0], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !mine, stopped = false;
         uint32_t ne = 0, nc = 0;
         const uint32_t s = rg.x + (uint32_t)k * L, e = min(rg.y, s + L);
-        walk<KIND, false>(rec, values, s, e, smem, st, ry, se, op, r, done, stopped, ne, nc);
+        walk<KIND, false>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, r, done, stopped, ne, nc);
         if (mine) {
             Acc a = {r.T, m[1 * npix] + r.A, m[2 * npix] + r.c0, m[3 * npix] + r.c1, m[4 * npix] + r.c2,
                      m[5 * npix] + r.d, m[6 * npix] + r.n0, m[7 * npix] + r.n1, m[8 * npix] + r.n2};
@@ -621,13 +784,15 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const uint32_t lfix = STATS ? 0x7fffffffu : (split_len > 0 ? (uint32_t)split_len : 0u);
     cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
     if (e != cudaSuccess) return e;
-    const size_t sm = (size_t)2 * npix * Rec<KIND>::S4 * 16;
+    const bool piped = npix > 32;   // multi-warp tiles: a producer warp + the staging ring
+    const size_t sm = (size_t)(piped ? KSLOTS : 2) * 32 * Rec<KIND>::S4 * 16;
+    const int nthr = piped ? npix + 32 : npix;
     e = cudaFuncSetAttribute(k_render<KIND, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, npix, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, nthr, sm);
     const unsigned ctas = (unsigned)std::max(1, nsm * std::max(per, 1));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)W.max_items));
     const unsigned gt = (unsigned)((ntiles + 255) / 256);
@@ -640,7 +805,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
-    k_render<KIND, STATS><<<grid, npix, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
+    k_render<KIND, STATS><<<grid, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
                                                   items, split_base, partials, o0, o1, o2, o3, stats, lfix, ctas);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -653,10 +818,10 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
         e = cudaFuncSetAttribute(k_rewalk<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         int per_rw = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_rw, k_rewalk<KIND>, npix, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_rw, k_rewalk<KIND>, nthr, sm);
         const unsigned grid_rw = (unsigned)std::max<int64_t>(
             1, std::min<int64_t>((int64_t)nsm * std::max(per_rw, 1), (int64_t)W.max_slots));
-        k_rewalk<KIND><<<grid_rw, npix, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_list,
+        k_rewalk<KIND><<<grid_rw, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_list,
                                                   mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
         e = cudaGetLastError();
     }
