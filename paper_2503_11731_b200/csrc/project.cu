@@ -207,24 +207,25 @@ struct AngBox {
 // Range of the linear-fractional f(c,s) = (n0 + n1 c + n2 s)/(d0 + d1 c + d2 s)
 // over the unit disk (denominator > 0 on it): the extremes lie on the circle
 // at the two roots of A c + B s + C = 0.
-__device__ void lf_range(double n0, double n1, double n2, double d0, double d1, double d2, double &lo,
-                         double &hi) {
+template <typename T>
+__device__ void lf_range(T n0, T n1, T n2, T d0, T d1, T d2, T &lo, T &hi) {
     lo = hi = n0 / d0;
-    const double A = n2 * d0 - n0 * d2, B = n0 * d1 - n1 * d0, C = n2 * d1 - n1 * d2;
-    const double rr = A * A + B * B;
-    if (rr > 0.0) {
-        const double q = sqrt(fmax(rr - C * C, 0.0));
-        const double cs[2][2] = {{(-A * C + B * q) / rr, (-B * C - A * q) / rr},
-                                 {(-A * C - B * q) / rr, (-B * C + A * q) / rr}};
+    const T A = n2 * d0 - n0 * d2, B = n0 * d1 - n1 * d0, C = n2 * d1 - n1 * d2;
+    const T rr = A * A + B * B;
+    if (rr > T(0)) {
+        const T q = sqrt(fmax(rr - C * C, T(0)));
+        const T irr = T(1) / rr;
+        const T cs[2][2] = {{(-A * C + B * q) * irr, (-B * C - A * q) * irr},
+                            {(-A * C - B * q) * irr, (-B * C + A * q) * irr}};
         for (int k = 0; k < 2; ++k) {
-            const double f = (n0 + n1 * cs[k][0] + n2 * cs[k][1]) / (d0 + d1 * cs[k][0] + d2 * cs[k][1]);
+            const T f = (n0 + n1 * cs[k][0] + n2 * cs[k][1]) / (d0 + d1 * cs[k][0] + d2 * cs[k][1]);
             lo = fmin(lo, f);
             hi = fmax(hi, f);
         }
     }
     for (int k = 0; k < 4; ++k) {   // safety points on the circle
-        const double c = k == 0 ? 1.0 : (k == 1 ? -1.0 : 0.0), s = k == 2 ? 1.0 : (k == 3 ? -1.0 : 0.0);
-        const double f = (n0 + n1 * c + n2 * s) / (d0 + d1 * c + d2 * s);
+        const T c = k == 0 ? T(1) : (k == 1 ? T(-1) : T(0)), s = k == 2 ? T(1) : (k == 3 ? T(-1) : T(0));
+        const T f = (n0 + n1 * c + n2 * s) / (d0 + d1 * c + d2 * s);
         lo = fmin(lo, f);
         hi = fmax(hi, f);
     }
@@ -272,6 +273,50 @@ __device__ bool angular_box_disk(const double mu[3], const double a[3], const do
     if (!ab.all_az) {
         ab.daz_hi = (double)atanf((float)(xh > 0.0 ? xh / Dlo : xh / Dhi)) + 5e-6;
         ab.daz_lo = (double)atanf((float)(xl < 0.0 ? xl / Dlo : xl / Dhi)) - 5e-6;
+    }
+    return true;
+}
+
+// The same bound in fp32 for well-conditioned disks (the disk keeps at least
+// 5% of the centre range away from the plane P.m = 0, so no quantity below is
+// amplified by more than ~20x), widened by margins far above fp32 error:
+// 1e-6 on the gnomonic coordinates, 4e-6 on the elevation sines, 8e-6 rad on
+// azimuth.  Only used for binning (it must contain the support; it need not
+// be tight to the last ulp).  Returns false -> use the fp64 version.
+__device__ bool angular_box_disk_f(const double mu[3], const double a_[3], const double b_[3], AngBox &ab) {
+    const double rd = sqrt(dot3(mu, mu));
+    const double ird = 1.0 / rd;
+    const float r = (float)rd;
+    const float m[3] = {(float)(mu[0] * ird), (float)(mu[1] * ird), (float)(mu[2] * ird)};
+    const float a[3] = {(float)a_[0], (float)a_[1], (float)a_[2]}, b[3] = {(float)b_[0], (float)b_[1], (float)b_[2]};
+    const float rho = sqrtf(m[0] * m[0] + m[1] * m[1]);
+    if (!(rho > 1e-3f)) return false;
+    const float irho = 1.f / rho;
+    const float eaz[3] = {-m[1] * irho, m[0] * irho, 0.f};
+    const float eel[3] = {-m[2] * m[0] * irho, -m[2] * m[1] * irho, rho};
+    const float d1 = a[0] * m[0] + a[1] * m[1] + a[2] * m[2], d2 = b[0] * m[0] + b[1] * m[1] + b[2] * m[2];
+    if (!(r - sqrtf(d1 * d1 + d2 * d2) > 0.05f * r)) return false;
+    float xl, xh, yl, yh;
+    lf_range(0.f, a[0] * eaz[0] + a[1] * eaz[1], b[0] * eaz[0] + b[1] * eaz[1], r, d1, d2, xl, xh);
+    lf_range(0.f, a[0] * eel[0] + a[1] * eel[1] + a[2] * eel[2], b[0] * eel[0] + b[1] * eel[1] + b[2] * eel[2], r,
+             d1, d2, yl, yh);
+    const float mgx = 1e-6f * (1.f + fabsf(xl) + fabsf(xh)), mgy = 1e-6f * (1.f + fabsf(yl) + fabsf(yh));
+    xl -= mgx; xh += mgx; yl -= mgy; yh += mgy;
+    const float x2lo = (xl <= 0.f && xh >= 0.f) ? 0.f : fminf(xl * xl, xh * xh), x2hi = fmaxf(xl * xl, xh * xh);
+    const float y2lo = (yl <= 0.f && yh >= 0.f) ? 0.f : fminf(yl * yl, yh * yh), y2hi = fmaxf(yl * yl, yh * yh);
+    const float den_lo = sqrtf(1.f + x2lo + y2lo), den_hi = sqrtf(1.f + x2hi + y2hi);
+    const float nlo = m[2] + yl * rho, nhi = m[2] + yh * rho;
+    const float shi = nhi > 0.f ? nhi / den_lo : nhi / den_hi;
+    const float slo = nlo > 0.f ? nlo / den_hi : nlo / den_lo;
+    ab.s_hi = (double)fminf(1.f, shi) + 4e-6;
+    ab.s_lo = (double)fmaxf(-1.f, slo) - 4e-6;
+    const float t1 = yl * m[2], t2 = yh * m[2];
+    const float Dlo = rho - fmaxf(t1, t2), Dhi = rho - fminf(t1, t2);
+    ab.azc = (double)atan2f(m[1], m[0]);
+    ab.all_az = !(Dlo > 1e-4f) || ab.s_hi >= 1.0 || ab.s_lo <= -1.0;
+    if (!ab.all_az) {
+        ab.daz_hi = (double)atanf(xh > 0.f ? xh / Dlo : xh / Dhi) + 8e-6;
+        ab.daz_lo = (double)atanf(xl < 0.f ? xl / Dlo : xl / Dhi) - 8e-6;
     }
     return true;
 }
@@ -380,24 +425,24 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
         }
     }
     // per round j: CTA-wide exclusive rank of this thread's item among the passing items of round j
-    __shared__ uint32_t s_round[SCAN_ITEMS][SCAN_THREADS / 32];
+    __shared__ unsigned long long s_round[SCAN_ITEMS * (SCAN_THREADS / 32)];   // [round][warp], 64 entries
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const uint32_t b = __ballot_sync(FULL_MASK, (flags >> j) & 1u);
-        if (lane == 0) s_round[j][warp] = __popc(b);
+        if (lane == 0) s_round[j * (SCAN_THREADS / 32) + warp] = __popc(b);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int j = 0; j < SCAN_ITEMS; ++j)
-            for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-                const uint32_t c = s_round[j][w];
-                s_round[j][w] = (uint32_t)tot;
-                tot += c;
-            }
-        const unsigned long long e = lookback_u64(st_cand, tile, tot);
-        s_excl = e;
-        if (base + SCAN_TILE >= s.n) hdr->n_cand = (uint32_t)(e + tot);
+    if (warp == 0) {
+        const unsigned long long t0 = warp_excl_scan_smem(s_round, 32);
+        const unsigned long long t1 = warp_excl_scan_smem(s_round + 32, 32);
+        if (lane < 32) s_round[32 + lane] += t0;
+        __syncwarp();
+        const unsigned long long tot = t0 + t1;
+        const unsigned long long e = lookback_warp_u64(st_cand, tile, tot);
+        if (lane == 0) {
+            s_excl = e;
+            if (base + SCAN_TILE >= s.n) hdr->n_cand = (uint32_t)(e + tot);
+        }
     }
     __syncthreads();
     const uint32_t lt = lanemask_lt();
@@ -405,7 +450,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const uint32_t b = __ballot_sync(FULL_MASK, (flags >> j) & 1u);
         if ((flags >> j) & 1u) {
-            const unsigned long long pos = s_excl + s_round[j][warp] + __popc(b & lt);
+            const unsigned long long pos = s_excl + s_round[j * (SCAN_THREADS / 32) + warp] + __popc(b & lt);
             cand[pos] = (uint32_t)(base + j * SCAN_THREADS + threadIdx.x);
         }
     }
@@ -489,7 +534,9 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             if (!whole) {
                 double a[3], b[3];
                 for (int k = 0; k < 3; ++k) { a[k] = Rr * su * A[k]; b[k] = Rr * sv * Bv[k]; }
-                if (!angular_box_disk(mu, a, b, ab, KIND == GS_FISHEYE_EQUIDISTANT)) angular_box_cap(m, asin(R3 / r), ab);
+                const bool fast = KIND == GS_LIDAR_SPINNING && angular_box_disk_f(mu, a, b, ab);
+                if (!fast && !angular_box_disk(mu, a, b, ab, KIND == GS_FISHEYE_EQUIDISTANT))
+                    angular_box_cap(m, asin(R3 / r), ab);
             }
             if (KIND == GS_FISHEYE_EQUIDISTANT) {
                 Box bx;
@@ -736,21 +783,19 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     unsigned long long ip = warp_inclusive_scan<unsigned long long>(lp);
     if (lane == 31) { s_wv[warp] = iv; s_wp[warp] = ip; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tv = 0, tp = 0;
-        for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-            const unsigned long long a = s_wv[w], b = s_wp[w];
-            s_wv[w] = tv; s_wp[w] = tp;
-            tv += a; tp += b;
-        }
-        const unsigned long long ev = lookback_u64(st_vis, tile, tv);
-        const unsigned long long ep = lookback_u64(st_pairs, tile, tp);
-        s_excl_v = ev;
-        const int64_t end = (int64_t)(tile + 1) * SCAN_TILE;
-        if (end >= n) {   // last tile: totals
-            hdr->n_visible = (uint32_t)(ev + tv);
-            hdr->num_pairs = (int64_t)(ep + tp);
-            if (d_num_pairs) *d_num_pairs = (int64_t)(ep + tp);
+    if (warp == 0) {
+        const unsigned long long tv = warp_excl_scan_smem(s_wv, SCAN_THREADS / 32);
+        const unsigned long long tp = warp_excl_scan_smem(s_wp, SCAN_THREADS / 32);
+        const unsigned long long ev = lookback_warp_u64(st_vis, tile, tv);
+        const unsigned long long ep = lookback_warp_u64(st_pairs, tile, tp);
+        if (lane == 0) {
+            s_excl_v = ev;
+            const int64_t end = (int64_t)(tile + 1) * SCAN_TILE;
+            if (end >= n) {   // last tile: totals
+                hdr->n_visible = (uint32_t)(ev + tv);
+                hdr->num_pairs = (int64_t)(ep + tp);
+                if (d_num_pairs) *d_num_pairs = (int64_t)(ep + tp);
+            }
         }
     }
     __syncthreads();

@@ -54,6 +54,64 @@ __device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *s
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+// Warp-parallel decoupled look-back: called by all 32 lanes of one warp with
+// the same `aggregate`.  Lane l inspects predecessor tile - 1 - l, so each
+// step covers 32 predecessors (one L2 round trip) instead of one.  Returns
+// the exclusive prefix (all lanes) and publishes the inclusive prefix.
+__device__ __forceinline__ unsigned long long lookback_warp_u64(unsigned long long *st, uint32_t tile,
+                                                               unsigned long long aggregate) {
+    const int lane = (int)(threadIdx.x & 31);
+    if (tile == 0) {
+        if (lane == 0) st_volatile_u64(&st[0], LB_PRE | aggregate);
+        return 0;
+    }
+    if (lane == 0) st_volatile_u64(&st[tile], LB_AGG | aggregate);
+    unsigned long long excl = 0;
+    int64_t base = (int64_t)tile - 1;
+    while (true) {
+        const int64_t idx = base - lane;
+        unsigned long long s = idx >= 0 ? ld_volatile_u64(&st[idx]) : LB_PRE;
+        while (__any_sync(FULL_MASK, (s >> 62) == 0))
+            if ((s >> 62) == 0) s = ld_volatile_u64(&st[idx]);
+        const uint32_t pre = __ballot_sync(FULL_MASK, (s >> 62) == 2);
+        unsigned long long v = s & LB_VAL;
+        if (pre) {
+            const int stop = __ffs(pre) - 1;   // nearest predecessor that holds an inclusive prefix
+            if (lane > stop) v = 0;
+            excl += warp_sum_u64(v);
+            break;
+        }
+        excl += warp_sum_u64(v);
+        base -= 32;
+    }
+    if (lane == 0) st_volatile_u64(&st[tile], LB_PRE | (excl + aggregate));
+    return excl;
+}
+
+// Exclusive scan of n <= 32 values v[0..n) held in shared memory, done by one
+// warp in place; returns the total (all lanes).
+__device__ __forceinline__ unsigned long long warp_excl_scan_smem(unsigned long long *v, int n) {
+    const int lane = (int)(threadIdx.x & 31);
+    const unsigned long long x = lane < n ? v[lane] : 0ull;
+    unsigned long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL_MASK, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const unsigned long long tot = __shfl_sync(FULL_MASK, inc, 31);
+    __syncwarp();
+    if (lane < n) v[lane] = inc - x;
+    __syncwarp();
+    return tot;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -250,20 +250,17 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_pair_offsets(
     const unsigned long long inc = warp_inclusive_scan<unsigned long long>(l);
     if (lane == 31) s_w[warp] = inc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-            const unsigned long long a = s_w[w];
-            s_w[w] = tot;
-            tot += a;
-        }
-        const unsigned long long e = lookback_u64(st, tile, tot);
-        s_excl = e;
-        if ((int64_t)(tile + 1) * SCAN_TILE >= (int64_t)n) {
-            const unsigned long long P = e + tot;
-            const bool over = (int64_t)P > cap || P >= (1ull << 30);
-            *d_overflow = over ? 1 : 0;
-            misc->n_pairs32 = over ? 0u : (uint32_t)P;
+    if (warp == 0) {
+        const unsigned long long tot = warp_excl_scan_smem(s_w, SCAN_THREADS / 32);
+        const unsigned long long e = lookback_warp_u64(st, tile, tot);
+        if (lane == 0) {
+            s_excl = e;
+            if ((int64_t)(tile + 1) * SCAN_TILE >= (int64_t)n) {
+                const unsigned long long P = e + tot;
+                const bool over = (int64_t)P > cap || P >= (1ull << 30);
+                *d_overflow = over ? 1 : 0;
+                misc->n_pairs32 = over ? 0u : (uint32_t)P;
+            }
         }
     }
     __syncthreads();
@@ -347,16 +344,38 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
 }
 
 // ------------------------------------------------------------------ ranges
+// Each thread scans 8 consecutive sorted keys (two 16-byte loads; the
+// neighbour on each side comes from the previous / next thread's registers
+// or one extra load at the warp edge) and writes the boundaries it sees.
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tkey, const SortMisc *misc,
                                                 uint32_t *__restrict__ ranges,
                                                 const int32_t *d_overflow) {
     if (*d_overflow) return;
     const uint32_t P = misc->n_pairs32;
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P) return;
-    const uint32_t t = tkey[i];
-    if (i == 0 || tkey[i - 1] != t) ranges[2 * t] = i;
-    if (i == P - 1 || tkey[i + 1] != t) ranges[2 * t + 1] = i + 1;
+    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (i0 >= P) return;
+    uint32_t k[8];
+    if (i0 + 8 <= P) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(tkey + i0));
+        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(tkey + i0) + 1);
+        k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) k[j] = i0 + j < P ? tkey[i0 + j] : 0xffffffffu;
+    }
+    uint32_t prev = i0 > 0 ? __ldg(tkey + i0 - 1) : 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t i = i0 + j;
+        if (i >= P) break;
+        if (k[j] != prev) {
+            ranges[2 * k[j]] = i;
+            if (i > 0) ranges[2 * prev + 1] = i;
+        }
+        prev = k[j];
+    }
+    const uint32_t last = min(i0 + 8, P);
+    if (last == P) ranges[2 * prev + 1] = P;
 }
 
 __global__ void __launch_bounds__(256) k_keys64(const uint32_t *__restrict__ tkey,
@@ -470,7 +489,8 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     // cur == 0 now: sorted tile keys in tk[0], values in `values`
     const unsigned gp = (unsigned)((cap + 255) / 256);
     note_launch();
-    k_ranges<<<gp > 0 ? gp : 1, 256, 0, st>>>(tk[cur], misc, ranges, d_overflow);
+    const unsigned gr = (unsigned)((cap + 2047) / 2048);
+    k_ranges<<<gr > 0 ? gr : 1, 256, 0, st>>>(tk[cur], misc, ranges, d_overflow);
     CK(cudaGetLastError());
     if (keys) {
         note_launch();

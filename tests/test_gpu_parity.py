@@ -196,3 +196,71 @@ def test_capacity_overflow_and_graph_mode(gsr_mod):
     big = r.render(c.sensors[0], capacity=P + 1000).cpu().numpy()
     assert not r.overflowed()
     np.testing.assert_array_equal(big, exact)
+
+
+# ---------------------------------------------------------------- batch / pipeline paths
+def test_batch_renderer_matches_single_frames(gsr_mod):
+    """BatchRenderer (capacity mode, two streams, per-frame overflow slots)
+    gives the same bytes as rendering each frame alone."""
+    from paper_2503_11731_b200.batch import BatchRenderer
+    from paper_2503_11731_b200.render import Renderer, to_device
+    rng = np.random.default_rng(41)
+    s = sg.street(rng, 40_000, 0.0, 60.0, 3, lidar_attrs=True)
+    sensors = [sg.pinhole(200, 120, 140.0, 100.0, 60.0, sg.camera_pose([0, 1.5, 10.0], np.deg2rad(y)))
+               for y in (0, 90, 180)]
+    sensors.append(sg.lidar64(sg.lidar_pose([0, 1.8, 10.0]), height=16, width=256))
+    dev = to_device(s)
+    br = BatchRenderer(dev, n_streams=2)
+    br.plan(sensors)
+    outs = br.alloc_outputs(br.wrap(sensors))
+    br.render(sensors, outs)
+    torch.cuda.synchronize()
+    assert br.overflowed() == []
+    single = Renderer(dev)
+    for se, o in zip(sensors, outs):
+        ref = single.render(se).cpu().numpy()
+        np.testing.assert_array_equal(o.cpu().numpy(), ref)
+
+
+def test_all_surfels_behind_camera_is_background(gsr_mod):
+    """Every surfel culled (none passes the cull): no candidates, no pairs."""
+    rng = np.random.default_rng(42)
+    s = sg.random_surfels(rng, 5000, [-3, -3, -9], [3, 3, -1], 0.05, 0.5, sh_degree=0)
+    se = sg.pinhole(64, 48, 50.0, 32.0, 24.0, sg.identity_pose())
+    img, r = _render(s, se)
+    assert r.last_pairs == 0
+    assert np.all(img == 0)
+
+
+@pytest.mark.parametrize("tiles", [(64, 4), (128, 2), (32, 8)])
+def test_lidar_tile_shape_invariance_bitwise(gsr_mod, tiles):
+    """LiDAR: one-warp tiles (self-staged) and multi-warp tiles (producer warp +
+    ring) composite identical per-ray sequences."""
+    rng = np.random.default_rng(43)
+    s = sg.street(rng, 40_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
+    se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=512)
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.render import Renderer, to_device
+    dev = to_device(s)
+    nosplit = gsr.default_opts(split_len=2 ** 31 - 1)
+    a = Renderer(dev, nosplit, lidar_tile=(32, 1)).render(se).cpu().numpy()
+    b = Renderer(dev, nosplit, lidar_tile=tiles).render(se).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+
+
+def test_early_stop_pipeline_long_lists(gsr_mod):
+    """Dense opaque layers: every ray saturates early in very long tile lists,
+    so the producer warp's STOP path runs; the result must still match the
+    oracle and the unsplit walk."""
+    rng = np.random.default_rng(44)
+    n = 60_000
+    s = sg.random_surfels(rng, n, [-2, -2, 2], [2, 2, 30], 0.2, 0.6, sh_degree=0)
+    s.opacities[:] = np.float32(0.95)
+    se = sg.pinhole(96, 64, 60.0, 48.0, 32.0, sg.identity_pose())
+    a, _ = _render(s, se, opts=dict(split_len=2 ** 31 - 1))
+    b, _ = _render(s, se)
+    assert np.abs(a - b).max() < 2e-5 * max(1.0, np.abs(a).max())
+    rays = parity.sample_rays(se, 1024, 4, tile=16)
+    ref, fl, _ = oracle.render(s, se, rays)
+    st = parity.compare(b, ref, fl, rays, se)
+    assert st["ok"], st
