@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
                                                        uint32_t *__restrict__ cand, unsigned long long *st_cand,
                                                        ProjHeader *hdr) {
     __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_w[SCAN_THREADS / 32], s_excl;
+    __shared__ unsigned long long s_excl;
     if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->cull_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -802,7 +802,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     unsigned long long pos = s_excl_v + s_wv[warp] + iv - lv;
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
-        const int64_t idx = base + j;
         if (c[j] > 0) {
             vkey[pos] = keys[id[j]];
             vid[pos] = id[j];

@@ -589,7 +589,7 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 // segment).  Unsplit tiles are written out; segments of split tiles leave
 // their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
-__global__ void __launch_bounds__(544) k_render(
+__global__ void __maxnreg__(80) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(512) k_merge_plan(
 // from each stopping sample's prefix transmittance; the segment's result is
 // added to the prefix composite and the sample written out.
 template <int KIND>
-__global__ void __launch_bounds__(544) k_rewalk(
+__global__ void __maxnreg__(80) k_rewalk(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
     SchedHdr *h, const uint32_t *__restrict__ split_list, const float *__restrict__ mstate,

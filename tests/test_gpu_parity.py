@@ -264,3 +264,53 @@ def test_early_stop_pipeline_long_lists(gsr_mod):
     ref, fl, _ = oracle.render(s, se, rays)
     st = parity.compare(b, ref, fl, rays, se)
     assert st["ok"], st
+
+
+def test_degenerate_surfels_edge_on_and_crossing_the_camera_plane(gsr_mod):
+    """Edge-on surfels (normal perpendicular to the view ray) and large surfels
+    straddling the camera plane z = 0 (their support is clipped by the near
+    plane; the pixel box comes from the near-plane chord) against the oracle,
+    full frame."""
+    rng = np.random.default_rng(45)
+    surfs = []
+    for _ in range(40):   # edge-on: normal along x, the surfel plane contains the view direction
+        R = np.array([[0.0, 0.0, 1.0], [0.0, 1.0, 0.0], [-1.0, 0.0, 0.0]])
+        surfs.append(dict(mu=rng.uniform([-1.5, -1, 2], [1.5, 1, 6]), R=R, s=(0.3, 0.2), o=0.8,
+                          rgb=rng.uniform(0, 1, 3)))
+    for _ in range(20):   # straddling z = 0: centre just in front, extent ~1 m along z
+        th = rng.uniform(0.3, 1.2)
+        R = np.array([[np.cos(th), 0.0, np.sin(th)], [0.0, 1.0, 0.0], [-np.sin(th), 0.0, np.cos(th)]])
+        surfs.append(dict(mu=[rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), rng.uniform(0.25, 0.6)],
+                          R=R.T, s=(0.6, 0.3), o=0.6, rgb=rng.uniform(0, 1, 3)))
+    s = scene(surfs)
+    se = sg.pinhole(96, 72, 60.0, 48.0, 36.0, sg.identity_pose())
+    _check(s, se, label="degenerate")
+
+
+@pytest.mark.slow
+def test_chunked_batch_sampled_bench_configuration(gsr_mod):
+    """The bench workload itself: BASELINE configs[4] (12 M surfels), frames of
+    timestep 32 rendered by BatchRenderer exactly as bench.py runs it (capacity
+    mode, two streams, 16x8 / 32x1 tiles), sampled rays vs the oracle."""
+    from paper_2503_11731_b200.batch import BatchRenderer
+    from paper_2503_11731_b200.render import to_device
+    s = sg.chunked_surfels()
+    sensors = sg.chunked_timestep_sensors(32)
+    frames = [sensors[0], sensors[1], sensors[6]]   # forward camera, side camera, LiDAR
+    br = BatchRenderer(to_device(s), n_streams=2)
+    br.plan(frames)
+    outs = br.alloc_outputs(br.wrap(frames))
+    br.render(frames, outs)
+    torch.cuda.synchronize()
+    assert br.overflowed() == []
+    # Surfels out to 400 m make ill-conditioned (far, tiny) intersections common:
+    # the oracle flags ~1 % of these rays (DESIGN.md §5), so the flagged-count
+    # bound is 2 % here; the strict 1e-4 gate on unflagged rays and the 0.02
+    # bound on flagged rays are unchanged.
+    for i, se in enumerate(frames):
+        rays = parity.sample_rays(se, 384, 1, tile=16, seed=i)
+        ref, fl, _ = oracle.render(s, se, rays)
+        st = parity.compare(outs[i].cpu().numpy(), ref, fl, rays, se)
+        print("chunked", i, {k: v for k, v in st.items() if k != "worst"})
+        assert st["bad"] == 0 and st["bad_flagged"] == 0, st
+        assert st["flagged"] <= max(2, 0.02 * st["n"]), st
