@@ -740,9 +740,9 @@ __global__ void __launch_bounds__(256, 3) k_project(DevSurfels s, const __grid_c
                                                  const uint32_t *__restrict__ cand, const ProjHeader *hdr,
                                                  float *__restrict__ rec, short4 *__restrict__ rect,
                                                  uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
-    const uint32_t nc = hdr->n_cand;
+    const uint32_t nc = cand ? hdr->n_cand : (uint32_t)s.n;   // no cand list: every surfel
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
-        project_one<KIND>(s, se, op, (int64_t)cand[c], rec, rect, keys, counts);
+        project_one<KIND>(s, se, op, cand ? (int64_t)cand[c] : (int64_t)c, rec, rect, keys, counts);
 }
 
 // ------------------------------------------------------------------ compaction
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(256, 3) k_project(DevSurfels s, const __grid_c
 // candidates; decoupled look-back.
 __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__restrict__ keys,
                                                           const uint32_t *__restrict__ counts,
-                                                          const uint32_t *__restrict__ cand,
+                                                          const uint32_t *__restrict__ cand, int64_t nsurf,
                                                           uint32_t *__restrict__ vkey,
                                                           uint32_t *__restrict__ vid,
                                                           unsigned long long *st_vis,
@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->scan_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const int64_t n = hdr->n_cand;
+    const int64_t n = cand ? (int64_t)hdr->n_cand : (int64_t)nsurf;
     if ((int64_t)tile * SCAN_TILE >= n && tile > 0) return;   // beyond the candidates: nobody looks back here
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)(warp * 32 + lane) * SCAN_ITEMS;
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const int64_t idx = base + j;
-        id[j] = idx < n ? cand[idx] : 0u;
+        id[j] = idx < n ? (cand ? cand[idx] : (uint32_t)idx) : 0u;
         c[j] = idx < n ? counts[id[j]] : 0u;
         lv += c[j] > 0 ? 1u : 0u;
         lp += c[j];
@@ -835,7 +835,7 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * 8);
-    note_launch(3);   // k_cull + k_project + k_compact
+    note_launch(se.kind == GS_LIDAR_SPINNING ? 2 : 3);   // [k_cull +] k_project + k_compact
     if (se.kind == GS_PINHOLE) {
         k_cull<GS_PINHOLE><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_PINHOLE><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
@@ -843,12 +843,14 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
         k_cull<GS_FISHEYE_EQUIDISTANT><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_FISHEYE_EQUIDISTANT><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
     } else {
-        k_cull<GS_LIDAR_SPINNING><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
+        // a spinning LiDAR sees all around: the conservative cull passes nearly every
+        // surfel, so skip it and project every surfel in index order (coalesced)
+        cand = nullptr;
         k_project<GS_LIDAR_SPINNING><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_compact<<<nblk, SCAN_THREADS, 0, st>>>(key, cnt, cand, (uint32_t *)(base + L.vkey), (uint32_t *)(base + L.vid),
+    k_compact<<<nblk, SCAN_THREADS, 0, st>>>(key, cnt, cand, s.n, (uint32_t *)(base + L.vkey), (uint32_t *)(base + L.vid),
                                             stv, stp, hdr, d_num_pairs);
     return cudaGetLastError();
 }

@@ -589,7 +589,7 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 // segment).  Unsplit tiles are written out; segments of split tiles leave
 // their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
-__global__ void __maxnreg__(80) k_render(
+__global__ void __maxnreg__(64) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,

@@ -144,6 +144,12 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
         k[j] = ok ? kin[idx] : 0xffffffffu;
         v[j] = ok ? vin[idx] : 0u;
     }
+    // Stable in-warp ranks: for item j the peers with the same digit come from
+    // one match; the leader reserves their slots with one shared atomicAdd
+    // (atomics of one warp to one address apply in program order, so item j's
+    // reservation precedes item j+1's) and broadcasts the old count.  The 16
+    // matches and atomics are independent, so they overlap instead of forming a
+    // load/store chain through shared memory.
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
@@ -151,12 +157,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
         const bool ok = idx < n;
         const uint32_t d = (k[j] >> shift) & mask;
         const uint32_t peers = __match_any_sync(FULL_MASK, ok ? d : 0x10000u);
-        const uint32_t before = __popc(peers & lt);
-        const uint32_t prev = ok ? whist[warp][d] : 0u;
-        __syncwarp();
-        if (ok && before == 0) whist[warp][d] = prev + __popc(peers);
-        __syncwarp();
-        rk[j] = prev + before;
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (ok && lane == leader) old = atomicAdd(&whist[warp][d], (uint32_t)__popc(peers));
+        rk[j] = __shfl_sync(FULL_MASK, old, leader) + __popc(peers & lt);
     }
     __syncthreads();
     // per digit: warp-exclusive offsets and tile count
