@@ -334,6 +334,34 @@ __device__ __forceinline__ void pipe_init(Pipe &pp, int nw) {
     __syncthreads();
 }
 
+// Evaluate the records of `buf` whose bit is set in the (warp-uniform) mask,
+// in order, for this lane's sample; stop at the first that ends the ray.
+// Records are taken in groups of four with compile-time offsets (empty groups
+// are skipped), which issues fewer instructions per record than a find-first-
+// set loop when the mask is dense and no more when it is sparse.
+template <int KIND, bool STATS>
+__device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restrict__ buf, const Ray &ry,
+                                          const DevOpts &op, Acc &a, bool &done, bool &stopped,
+                                          uint32_t &n_eval, uint32_t &n_comp) {
+    constexpr int S4 = Rec<KIND>::S4;
+#pragma unroll 1
+    for (int jj = 0; jj < 32; jj += 4) {
+        const uint32_t nib = (bits >> jj) & 0xfu;
+        if (!nib) continue;
+        const float4 *b4 = buf + jj * S4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (nib & (1u << u)) {
+                if (!eval_record<KIND, STATS>(b4 + u * S4, ry, op, a, n_eval, n_comp)) {
+                    done = true;
+                    stopped = true;
+                    return;
+                }
+            }
+        }
+    }
+}
+
 // CTA walk of list entries [s, e) of `values`; every thread of the CTA calls
 // it.  Consumer thread: its sample `ry` in its warp's sub-tile `st`; `done`
 // lanes skip work and a lane becomes done when its ray stops (`stopped`).
@@ -392,18 +420,8 @@ __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const 
                     const float4 bb = buf[lane * S4 + BB4];
                     hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
                 }
-                uint32_t bits = __ballot_sync(FULL, hit);
-                if (bits && !done) {
-                    do {
-                        const int j = __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        if (!eval_record<KIND, STATS>(buf + j * S4, ry, op, a, n_eval, n_comp)) {
-                            done = true;
-                            stopped = true;
-                            break;
-                        }
-                    } while (bits);
-                }
+                const uint32_t bits = __ballot_sync(FULL, hit);
+                if (bits && !done) eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
                 if (__all_sync(FULL, done)) {
                     wdone = true;
                     if (lane == 0) atomicAdd(&pp.n_done, 1);
@@ -456,18 +474,8 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
             const float4 bb = buf[lane * S4 + BB4];
             hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
         }
-        uint32_t bits = __ballot_sync(FULL, hit);
-        if (bits && !done) {
-            do {
-                const int j = __ffs(bits) - 1;
-                bits &= bits - 1;
-                if (!eval_record<KIND, STATS>(buf + j * S4, ry, op, a, n_eval, n_comp)) {
-                    done = true;
-                    stopped = true;
-                    break;
-                }
-            } while (bits);
-        }
+        const uint32_t bits = __ballot_sync(FULL, hit);
+        if (bits && !done) eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
         if (__all_sync(FULL, done)) break;
         __syncwarp();
     }
