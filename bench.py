@@ -399,7 +399,7 @@ def main():
     ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
     ap.add_argument("--workload", default="chunked", choices=["chunked", "mid", "fisheye", "lidar", "tiny"])
     ap.add_argument("--timesteps", type=int, default=64)
-    ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--streams", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
