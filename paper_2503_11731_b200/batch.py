@@ -29,6 +29,16 @@ class FrameTimes:
     sort: list = field(default_factory=list)
     render: list = field(default_factory=list)
 
+    @staticmethod
+    def from_events(evs) -> "FrameTimes":
+        """Durations from recorded (completed) per-frame event quadruples."""
+        t = FrameTimes()
+        for ev in evs:
+            t.project.append(ev[0].elapsed_time(ev[1]))
+            t.sort.append(ev[1].elapsed_time(ev[2]))
+            t.render.append(ev[2].elapsed_time(ev[3]))
+        return t
+
 
 class BatchRenderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
@@ -72,11 +82,14 @@ class BatchRenderer:
         torch.cuda.synchronize(self.device)
         return (caps, contrib, evals) if stats else caps
 
-    def render(self, sensors, outs, times: FrameTimes | None = None, on_frame=None):
+    def render(self, sensors, outs, times: FrameTimes | None = None, on_frame=None, event_log: list | None = None):
         """Render frame i into outs[i] on lane i % n_streams.  times: if given,
         per-frame event durations are appended after the batch completes
-        (this synchronises).  on_frame(i, stream): called right after frame i
-        is enqueued (e.g. to chain a device->host copy)."""
+        (this synchronises).  event_log: if given, each frame's 4 CUDA events
+        (before gs_project, gs_bin_sort, the render call, after it) are
+        appended without synchronising (read them after a later sync, e.g.
+        with FrameTimes.from_events).  on_frame(i, stream): called right after
+        frame i is enqueued (e.g. to chain a device->host copy)."""
         sensors = self.wrap(sensors)
         assert self.caps is not None and len(self.caps) == len(sensors), "call plan() first"
         cur = torch.cuda.current_stream(self.device)
@@ -85,13 +98,16 @@ class BatchRenderer:
         evs = []
         for i, s in enumerate(sensors):
             k = i % len(self.lanes)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if times is not None else None
+            want = times is not None or event_log is not None
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if want else None
             with torch.cuda.stream(self.streams[k]):
                 self.lanes[k].render(s, out=outs[i], capacity=self.caps[i], events=ev,
                                      overflow=self.ovf[i:i + 1])
                 if on_frame is not None:
                     on_frame(i, self.streams[k])
             evs.append(ev)
+        if event_log is not None:
+            event_log.extend(evs)
         for st in self.streams:
             cur.wait_stream(st)
         if times is not None:
