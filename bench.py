@@ -191,6 +191,58 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ per-config single-frame rates
+def measure_configs(device, names=("tiny", "mid", "fisheye", "lidar"), min_ms=300.0):
+    """Single-frame throughput of the other BASELINE configs (per GPU): the
+    frame's whole path (gs_project -> gs_bin_sort -> render) captured once in a
+    CUDA graph (capacity mode, no host sync) and replayed back to back, timed
+    with CUDA events.  Returns {name: {...}}."""
+    import torch
+
+    import scenegen as sg
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.render import Renderer, to_device
+    res = {}
+    for name in names:
+        c = sg.make_config(name)
+        se = gsr.Sensor(c.sensors[0])
+        r = Renderer(to_device(c.surfels, device))
+        out = r.render(se)            # exact sizing once
+        cap = r.last_pairs
+        s = torch.cuda.Stream(device)
+        s.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                r.render(se, out=out, capacity=cap)
+        torch.cuda.current_stream(device).wait_stream(s)
+        torch.cuda.synchronize(device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            r.render(se, out=out, capacity=cap)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g.replay()
+        torch.cuda.synchronize(device)
+        reps = 5
+        while True:
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize(device)
+            ms = a.elapsed_time(b)
+            if ms >= min_ms or reps >= 20000:
+                break
+            reps = int(reps * max(2.0, 1.2 * min_ms / max(ms, 1e-3)))
+        assert not r.overflowed()
+        per = ms / reps
+        samples = se.width * se.height
+        res[name] = {"value": round(samples / (per * 1e-3) / 1e6, 2), "unit": UNIT, "ms_per_frame": round(per, 4),
+                     "surfels": c.surfels.n, "frame": f"{se.width}x{se.height} kind {se.kind}", "pairs": cap,
+                     "reps": reps, "how": "whole path captured in a CUDA graph, replayed back to back"}
+        del r, g
+    return res
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_gsr(args):
     import torch
@@ -250,7 +302,43 @@ def run_gsr(args):
         for r in reqs:
             r.wait()
 
+    per_step_t = len(groups[0])
+    cur = torch.cuda.current_stream(device)
+    comm = torch.cuda.Stream(device) if world > 1 else None
+    local_blocks = {k: slabs_local[k].view(hi - lo, sum(1 for s in groups[0] if int(s.kind) == k),
+                                           *slabs_local[k].shape[1:]) for k in kinds}
+    full_blocks = ({k: slabs_full[k].view(n_steps_t, sum(1 for s in groups[0] if int(s.kind) == k),
+                                          *slabs_full[k].shape[1:]) for k in kinds} if rank == 0 else None)
+
     def step(times=None, on_frame=None, event_log=None):
+        if world > 1 and args.gather == "rounds":
+            # post gather round j (this rank's j-th timestep) as soon as its frames are enqueued
+            reqs = []
+            import torch.distributed as dist
+
+            def post(i, st):
+                if on_frame is not None:
+                    on_frame(i, st)
+                if i % per_step_t != per_step_t - 1:
+                    return
+                j = i // per_step_t
+                for lane_st in br.streams:
+                    comm.wait_stream(lane_st)
+                ops = gd.round_ops(local_blocks, full_blocks, j, n_steps_t, world, rank)
+                with torch.cuda.stream(comm):
+                    if ops:
+                        reqs.extend(dist.batch_isend_irecv(ops))
+            br.render(sensors, outs, times=times, on_frame=post, event_log=event_log)
+            if rank == 0:   # rounds the root has no timestep for (uneven blocks) still receive
+                for j in range(hi - lo, gd.n_rounds(n_steps_t, world)):
+                    ops = gd.round_ops(local_blocks, full_blocks, j, n_steps_t, world, rank)
+                    with torch.cuda.stream(comm):
+                        if ops:
+                            reqs.extend(dist.batch_isend_irecv(ops))
+            for r in reqs:
+                r.wait()
+            cur.wait_stream(comm)
+            return
         br.render(sensors, outs, times=times, on_frame=on_frame, event_log=event_log)
         gather()
 
@@ -387,6 +475,9 @@ def run_gsr(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(surfels_np, all_sensors, args.cpu_seconds)
+    per_config = None
+    if rank == 0 and not args.no_configs:
+        per_config = measure_configs(device)
 
     if rank == 0:
         desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
@@ -400,7 +491,7 @@ def run_gsr(args):
                 "BASELINE.json configs; random surfels, no trained scene)", "config": desc,
                 "e2e": e2e, "gpu_launches": int(n_launch), "gpu_launches_per_step": n_launch // args.steps,
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "stages": stage,
-                "setup_s": {"generate": round(t_gen, 1)}}
+                "per_config": per_config, "setup_s": {"generate": round(t_gen, 1)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -419,6 +510,10 @@ def main():
     ap.add_argument("--streams", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-frame rates")
+    ap.add_argument("--gather", choices=["end", "rounds"], default="end",
+                    help="N > 1: gather all frames after the batch (end) or one timestep round at a time as "
+                         "soon as it is rendered, overlapping the transfer with rendering (rounds)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-rays", type=int, default=256)
     args = ap.parse_args()

@@ -102,3 +102,35 @@ def barrier(world: int, device=None):
             dist.barrier(device_ids=[device.index])
         else:
             dist.barrier()
+
+
+def round_ops(local: dict, full: dict | None, j: int, n_items: int, world: int, rank: int, root: int = 0,
+              group=None):
+    """Point-to-point ops of gather round j: every non-root rank sends the j-th
+    item of its block (one tensor per key of `local`, e.g. the camera and the
+    LiDAR frames of its j-th timestep) and the root receives item j of every
+    peer's block straight into its slot of `full`.  All ranks issue the rounds
+    in the same order, so each round's sends and receives match one to one;
+    posting round j as soon as item j is rendered overlaps the transfer with
+    the rendering of the next items."""
+    ops = []
+    if world == 1:
+        return ops
+    if rank == root:
+        for r in range(world):
+            if r == root:
+                continue
+            lo, hi = shard_range(n_items, world, r)
+            if j < hi - lo:
+                for k in sorted(full):
+                    ops.append(dist.P2POp(dist.irecv, full[k][lo + j], r, group))
+    else:
+        lo, hi = shard_range(n_items, world, rank)
+        if j < hi - lo:
+            for k in sorted(local):
+                ops.append(dist.P2POp(dist.isend, local[k][j], root, group))
+    return ops
+
+
+def n_rounds(n_items: int, world: int) -> int:
+    return max(shard_counts(n_items, world)) if world > 0 else 0

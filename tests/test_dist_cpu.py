@@ -87,3 +87,49 @@ def test_gather_world1_copies():
     full = torch.zeros(3, 4)
     assert gd.gather_blocks(local, full, 3, 1, 0) == []
     assert torch.equal(full, local)
+
+
+def _round_worker(rank, world, port, n_t, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        shapes = {"cam": (6, 2, 3, 4), "lidar": (1, 4, 2, 5)}
+        lo, hi = gd.shard_range(n_t, world, rank)
+        full = {k: torch.full((n_t,) + sh, -1.0) for k, sh in shapes.items()} if rank == 0 else None
+        local = {k: (full[k][lo:hi] if rank == 0 else torch.empty((hi - lo,) + sh)) for k, sh in shapes.items()}
+        reqs = []
+        for j in range(gd.n_rounds(n_t, world)):
+            if j < hi - lo:   # "render" item j of this rank's block, then post its round
+                for k, sh in shapes.items():
+                    local[k][j] = _frame(lo + j, sh) + (0.5 if k == "lidar" else 0.0)
+            ops = gd.round_ops(local, full, j, n_t, world, rank)
+            if ops:
+                reqs += dist.batch_isend_irecv(ops)
+        for r in reqs:
+            r.wait()
+        if rank == 0:
+            ok = all(torch.equal(full[k][t], _frame(t, sh) + (0.5 if k == "lidar" else 0.0))
+                     for k, sh in shapes.items() for t in range(n_t))
+            q.put(("ok", ok, None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), None))
+
+
+@pytest.mark.parametrize("world,n_t", [(2, 8), (3, 7), (4, 6)])
+def test_overlapped_gather_rounds_gloo(world, n_t):
+    """Round-wise gather (post item j as soon as it is rendered) assembles the
+    same batch on rank 0, uneven blocks included."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_round_worker, args=(r, world, port, n_t, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == "ok" and res[1], res
+    assert all(p.exitcode == 0 for p in ps)
