@@ -1,8 +1,9 @@
 """Sweep render settings (tile shape, warp layout, split length) per frame (dev tool).
 
-python tools/sweep.py <config> [cam_tiles] [lidar_tiles] [layouts] [split_lens]
+python tools/sweep.py <config> [cam_tiles] [lidar_tiles] [unused] [split_lens]
   config: mid fisheye lidar tiny chunked (chunked: t=32 forward, side, LiDAR)
-  cam_tiles / lidar_tiles: e.g. 16x16,32x16 ; layouts: 0,1 ; split_lens: 0,4096
+  cam_tiles / lidar_tiles: e.g. 16x16,32x16 ; split_lens: 0,4096 (0 = adaptive)
+  (the fourth argument once selected an experimental warp layout; it is ignored)
 Prints one JSON line per (frame, setting): ms per stage (median of 5).
 """
 import json
@@ -45,7 +46,6 @@ def main():
         for (tw, th) in tiles:
             for lay in layouts:
                 for L in splits:
-                    os.environ["GSR_LAYOUT"] = str(lay)
                     opts = gsr.default_opts(tile_w=tw, tile_h=th, split_len=L)
                     r = Renderer(dev, opts, lidar_tile=(tw, th))
                     out = r.render(gs)
