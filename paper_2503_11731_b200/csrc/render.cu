@@ -55,6 +55,8 @@ constexpr float LOG2E_HALF = 0.72134752044448170368f;   // 0.5 * log2(e)
 constexpr int NB = 32;                                   // schedule buckets
 constexpr int NPART = 10;                                // floats per partial composite
 constexpr uint32_t LMIN = 1024;   // shortest segment of the adaptive split (workspace sizing)
+constexpr int NCP = 4;            // checkpoints per split segment (the re-walk covers one fifth)
+constexpr uint32_t NO_STOP = 0xffffffffu;
 constexpr unsigned FULL = 0xffffffffu;
 
 // F: floats per record; BB: float index of the packed pixel box; S4: record
@@ -82,7 +84,7 @@ struct SchedHdr {
 static_assert(sizeof(SchedHdr) == 384, "hdr");
 
 struct RenderWs {
-    size_t hdr, items, split_base, split_list, partials, mstate, rw_items, total;
+    size_t hdr, items, split_base, split_list, partials, mstate, rw_items, ckpt, total;
     uint32_t max_items, max_split, max_slots, L;
     RenderWs(int64_t cap, int64_t ntiles, int32_t split_len, int npix) {
         L = split_len > 0 ? (uint32_t)split_len : LMIN;
@@ -98,6 +100,7 @@ struct RenderWs {
         partials = o; o += align256((size_t)max_slots * NPART * npix * 4);
         mstate = o; o += align256((size_t)max_split * NPART * npix * 4);
         rw_items = o; o += align256((size_t)max_slots * 8);
+        ckpt = o; o += align256((size_t)max_slots * NCP * NPART * npix * 4);
         total = o;
     }
 };
@@ -276,6 +279,33 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
     return true;
 }
 
+// Segment checkpoints: a split segment's walk leaves its local composite after
+// every CB batches (NCP of them, SoA like the partials) so that the exact-stop
+// re-walk can start from the last checkpoint before the stop instead of the
+// segment start.  The slot's last float is unused (the stop batch lives in
+// the partial).
+struct Ckpt {
+    float *base;     // this segment's NCP checkpoint blocks, or nullptr
+    uint32_t cb;     // batches between checkpoints
+    int npix, t;     // samples per tile, this thread's sample
+};
+
+__device__ __forceinline__ void ckpt_store(const Ckpt &ck, uint32_t b_done, uint32_t nb, const Acc &a) {
+    // b_done batches have been walked; checkpoint c sits at c * cb batches
+    if (!ck.base || b_done % ck.cb != 0u || b_done >= nb) return;
+    const uint32_t c = b_done / ck.cb;
+    if (c < 1u || c > (uint32_t)NCP) return;
+    float *p = ck.base + (size_t)(c - 1) * NPART * ck.npix + ck.t;
+    const int n = ck.npix;
+    p[0 * n] = a.T; p[1 * n] = a.A; p[2 * n] = a.c0; p[3 * n] = a.c1; p[4 * n] = a.c2;
+    p[5 * n] = a.d; p[6 * n] = a.n0; p[7 * n] = a.n1; p[8 * n] = a.n2;
+}
+
+__device__ __forceinline__ uint32_t ckpt_batches(uint32_t L) {   // cb for segment length L
+    const uint32_t nb = (L + 31) >> 5;
+    return (nb + NCP) / (NCP + 1);
+}
+
 // ---------------------------------------------------------------- staging pipeline
 // Warp-specialised: the last warp of the CTA is the producer -- it copies the
 // depth-sorted records of the tile list into a ring of KSLOTS slots (32
@@ -371,7 +401,8 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *ring, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
-                                     Acc &a, bool &done, bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
+                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, const Ckpt &ck,
+                                     uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5) - 1;
@@ -421,12 +452,16 @@ __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const 
                     hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
                 }
                 const uint32_t bits = __ballot_sync(FULL, hit);
-                if (bits && !done) eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
+                if (bits && !done) {
+                    eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
+                    if (stopped && stop_b == NO_STOP) stop_b = b;
+                }
                 if (__all_sync(FULL, done)) {
                     wdone = true;
                     if (lane == 0) atomicAdd(&pp.n_done, 1);
                 }
             }
+            if (cnt >= 0) ckpt_store(ck, b + 1, nb, a);
             __syncwarp();
             if (lane == 0) mbar_arrive(&pp.empty[slot]);
             if (cnt < 0) { used = b + 1; break; }
@@ -442,7 +477,8 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                           uint32_t s, uint32_t e, float4 *buf2, const SubTile &st, const Ray &ry,
                                           const DevSensor &se, const DevOpts &op, Acc &a, bool &done,
-                                          bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
+                                          bool &stopped, uint32_t &stop_b, const Ckpt &ck, uint32_t &n_eval,
+                                          uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
     const int lane = threadIdx.x & 31;
@@ -475,8 +511,12 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
             hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
         }
         const uint32_t bits = __ballot_sync(FULL, hit);
-        if (bits && !done) eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
-        if (__all_sync(FULL, done)) break;
+        if (bits && !done) {
+            eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
+            if (stopped && stop_b == NO_STOP) stop_b = b;
+        }
+        if (__all_sync(FULL, done)) break;   // every later checkpoint is past every stop: never read
+        ckpt_store(ck, b + 1, nb, a);
         __syncwarp();
     }
     cp_async_wait<0>();
@@ -487,11 +527,14 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk(bool piped, const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *smem, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
-                                     Acc &a, bool &done, bool &stopped, uint32_t &n_eval, uint32_t &n_comp) {
+                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, const Ckpt &ck,
+                                     uint32_t &n_eval, uint32_t &n_comp) {
     if (piped)
-        walk_pipe<KIND, STATS>(rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+        walk_pipe<KIND, STATS>(rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
+                               n_eval, n_comp);
     else
-        walk_self<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+        walk_self<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, stop_b, ck, n_eval,
+                               n_comp);
 }
 
 template <int KIND>
@@ -602,9 +645,10 @@ __global__ void __maxnreg__(64) k_render(
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
-    float *__restrict__ partials, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
     const uint32_t L = seg_len(h, lfix, ctas);
+    const uint32_t cb = ckpt_batches(L);
     extern __shared__ float4 smem[];
     __shared__ uint32_t s_item;
     __shared__ Pipe pp;
@@ -633,8 +677,11 @@ __global__ void __maxnreg__(64) k_render(
         const Ray ry = make_ray<KIND>(se, st, lane);
         Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !ry.valid, stopped = false;
-        uint32_t n_eval = 0, n_comp = 0;
-        walk<KIND, STATS>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, n_eval, n_comp);
+        uint32_t n_eval = 0, n_comp = 0, stop_b = NO_STOP;
+        Ckpt ck = {nullptr, cb, npix, t};
+        if (ns > 1 && cons) ck.base = ckpt + (size_t)(split_base[tile] + seg) * NCP * NPART * npix;
+        walk<KIND, STATS>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
+                          n_eval, n_comp);
         if (!cons) continue;
         if (ns == 1) {
             write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
@@ -647,7 +694,7 @@ __global__ void __maxnreg__(64) k_render(
             float *p = partials + (size_t)(split_base[tile] + seg) * NPART * npix + t;
             p[0 * npix] = a.T; p[1 * npix] = a.A; p[2 * npix] = a.c0; p[3 * npix] = a.c1;
             p[4 * npix] = a.c2; p[5 * npix] = a.d; p[6 * npix] = a.n0; p[7 * npix] = a.n1;
-            p[8 * npix] = a.n2; p[9 * npix] = stopped ? 1.f : 0.f;
+            p[8 * npix] = a.n2; p[9 * npix] = __uint_as_float(stopped ? stop_b + 1u : 0u);   // 0 = no local stop
         }
     }
 }
@@ -665,9 +712,11 @@ template <int KIND>
 __global__ void __launch_bounds__(512) k_merge_plan(
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
     SchedHdr *h, const uint32_t *__restrict__ split_base, const uint32_t *__restrict__ split_list,
-    const float *__restrict__ partials, float *__restrict__ mstate, uint2 *__restrict__ rw_items,
-    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
+    const float *__restrict__ partials, const float *__restrict__ ckpt, float *__restrict__ mstate,
+    uint2 *__restrict__ rw_items, float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2,
+    float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
     const uint32_t L = seg_len(h, lfix, ctas);
+    const uint32_t cb = ckpt_batches(L);
     if (blockIdx.x >= h->n_split) return;
     const int tile = (int)split_list[blockIdx.x];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, npix = blockDim.x;
@@ -680,7 +729,7 @@ __global__ void __launch_bounds__(512) k_merge_plan(
     for (uint32_t k = 0; k < ns; ++k) {
         const float *p = partials + (size_t)(base + k) * NPART * npix + t;
         const float Tk = p[0];
-        const bool stop_k = p[9 * npix] != 0.f;
+        const bool stop_k = __float_as_uint(p[9 * npix]) != 0u;
         if (!stop_k && a.T * Tk >= op.t_min) {
             const float Tr = a.T;
             a.A = fmaf(Tr, p[1 * npix], a.A); a.c0 = fmaf(Tr, p[2 * npix], a.c0);
@@ -698,16 +747,44 @@ __global__ void __launch_bounds__(512) k_merge_plan(
         }
     }
     if (!ry.valid) kstar = -1;
+    int tag = -1;   // (k*, c): re-walk segment k* from its checkpoint c (0 = the segment start)
     if (kstar < 0) {
         write_final<KIND>(se, op, ry, a, o0, o1, o2, o3);
+    } else {
+        // advance to the last checkpoint c of segment k* that precedes both the local stop
+        // (c cb <= stop batch) and the global one (T_run T_c >= t_min): the ray is still
+        // running there, so the prefix composite extends exactly to it
+        const uint32_t k = (uint32_t)kstar;
+        const float *p = partials + (size_t)(base + k) * NPART * npix + t;
+        const uint32_t sb = __float_as_uint(p[9 * npix]);   // local stop batch + 1, 0 = none
+        const uint32_t seg_s = rg.x + k * L, seg_e = min(rg.y, seg_s + L), nb = (seg_e - seg_s + 31) >> 5;
+        const float Tr = a.T;
+        int c = 0;
+        for (int cc = 1; cc <= NCP; ++cc) {
+            const uint32_t at = (uint32_t)cc * cb;
+            if (at >= nb || (sb != 0u && at > sb - 1u)) break;
+            const float *q = ckpt + ((size_t)(base + k) * NCP + (cc - 1)) * NPART * npix + t;
+            if (!(Tr * q[0] >= op.t_min)) break;
+            c = cc;
+        }
+        if (c > 0) {
+            const float *q = ckpt + ((size_t)(base + k) * NCP + (c - 1)) * NPART * npix + t;
+            a.A = fmaf(Tr, q[1 * npix], a.A); a.c0 = fmaf(Tr, q[2 * npix], a.c0);
+            a.c1 = fmaf(Tr, q[3 * npix], a.c1); a.c2 = fmaf(Tr, q[4 * npix], a.c2);
+            a.d = fmaf(Tr, q[5 * npix], a.d); a.n0 = fmaf(Tr, q[6 * npix], a.n0);
+            a.n1 = fmaf(Tr, q[7 * npix], a.n1); a.n2 = fmaf(Tr, q[8 * npix], a.n2);
+            a.T = Tr * q[0];
+        }
+        tag = kstar | (c << 24);
     }
     float *m = mstate + (size_t)blockIdx.x * NPART * npix + t;
     m[0 * npix] = a.T; m[1 * npix] = a.A; m[2 * npix] = a.c0; m[3 * npix] = a.c1; m[4 * npix] = a.c2;
     m[5 * npix] = a.d; m[6 * npix] = a.n0; m[7 * npix] = a.n1; m[8 * npix] = a.n2;
-    m[9 * npix] = __int_as_float(kstar);
+    m[9 * npix] = __int_as_float(tag);
     for (uint32_t k = 0; k < ns; ++k)
-        if (__syncthreads_or(kstar == (int)k) && t == 0)
-            rw_items[atomicAdd(&h->rw_count, 1u)] = make_uint2(blockIdx.x, k);
+        for (int c = 0; c <= NCP; ++c)
+            if (__syncthreads_or(tag == (int)(k | ((uint32_t)c << 24))) && t == 0)
+                rw_items[atomicAdd(&h->rw_count, 1u)] = make_uint2(blockIdx.x, k | ((uint32_t)c << 24));
 }
 
 // Persistent CTAs over the re-walk items: segment k of split tile s is walked
@@ -721,6 +798,7 @@ __global__ void __maxnreg__(80) k_rewalk(
     const uint2 *__restrict__ rw_items, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
     const uint32_t L = seg_len(h, lfix, ctas);
+    const uint32_t cb = ckpt_batches(L);
     extern __shared__ float4 smem[];
     __shared__ uint32_t s_item;
     __shared__ Pipe pp;
@@ -739,17 +817,20 @@ __global__ void __maxnreg__(80) k_rewalk(
         if (item >= n_items) break;
         const uint2 it = rw_items[item];
         const int tile = (int)split_list[it.x];
-        const int k = (int)it.y;
+        const uint32_t k = it.y & 0xffffffu, c = it.y >> 24;
         const uint2 rg = ranges[tile];
         const SubTile st = sub_tile(se, tile, warp);
         const Ray ry = make_ray<KIND>(se, st, lane);
         const float *m = mstate + (size_t)it.x * NPART * npix + (cons ? t : 0);
-        const bool mine = cons && __float_as_int(m[9 * npix]) == k;
+        const bool mine = cons && __float_as_uint(m[9 * npix]) == it.y;
         Acc r = {m[0], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !mine, stopped = false;
-        uint32_t ne = 0, nc = 0;
-        const uint32_t s = rg.x + (uint32_t)k * L, e = min(rg.y, s + L);
-        walk<KIND, false>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, r, done, stopped, ne, nc);
+        uint32_t ne = 0, nc = 0, sb = NO_STOP;
+        const Ckpt ck = {nullptr, 1u, npix, t};
+        // the chunk between checkpoints c and c+1 of segment k (the ray stops inside it)
+        const uint32_t seg_s = rg.x + k * L, seg_e = min(rg.y, seg_s + L);
+        const uint32_t s = min(seg_e, seg_s + c * cb * 32u), e = min(seg_e, seg_s + (c + 1u) * cb * 32u);
+        walk<KIND, false>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, r, done, stopped, sb, ck, ne, nc);
         if (mine) {
             Acc a = {r.T, m[1 * npix] + r.A, m[2 * npix] + r.c0, m[3 * npix] + r.c1, m[4 * npix] + r.c2,
                      m[5 * npix] + r.d, m[6 * npix] + r.n0, m[7 * npix] + r.n1, m[8 * npix] + r.n2};
@@ -788,6 +869,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     uint2 *items = (uint2 *)(wb + W.items);
     uint32_t *split_base = (uint32_t *)(wb + W.split_base), *split_list = (uint32_t *)(wb + W.split_list);
     float *partials = (float *)(wb + W.partials);
+    float *ckpt = (float *)(wb + W.ckpt);
     // instrumented runs are never split; split_len > 0 fixes the segment length
     const uint32_t lfix = STATS ? 0x7fffffffu : (split_len > 0 ? (uint32_t)split_len : 0u);
     cudaError_t e = cudaMemsetAsync(h, 0, sizeof(SchedHdr), st);
@@ -814,7 +896,8 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     if (e != cudaSuccess) return e;
     note_launch();
     k_render<KIND, STATS><<<grid, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
-                                                  items, split_base, partials, o0, o1, o2, o3, stats, lfix, ctas);
+                                                  items, split_base, partials, ckpt, o0, o1, o2, o3, stats, lfix,
+                                                  ctas);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!STATS && W.max_split > 0) {
@@ -822,7 +905,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
         uint2 *rw_items = (uint2 *)(wb + W.rw_items);
         note_launch(2);
         k_merge_plan<KIND><<<W.max_split, npix, 0, st>>>((const uint2 *)ranges, se, op, h, split_base, split_list,
-                                                         partials, mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
+                                                         partials, ckpt, mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
         e = cudaFuncSetAttribute(k_rewalk<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         int per_rw = 1;

@@ -133,10 +133,12 @@ def test_tile_shape_invariance_bitwise(gsr_mod, tiles):
     np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("split", [16, 160, 480])
 @pytest.mark.parametrize("cfg", ["street", "fisheye", "lidar"])
-def test_split_lists_match_unsplit_and_oracle(gsr_mod, cfg):
-    """Segmented compositing + transmittance-prefix merge (exact stop rule)
-    agrees with the sequential walk to fp32 rounding and passes the oracle gate."""
+def test_split_lists_match_unsplit_and_oracle(gsr_mod, cfg, split):
+    """Segmented compositing + transmittance-prefix merge (exact stop rule, the
+    re-walk starting from the last segment checkpoint before the stop) agrees
+    with the sequential walk to fp32 rounding and passes the oracle gate."""
     rng = np.random.default_rng(31)
     if cfg == "street":
         c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
@@ -149,7 +151,7 @@ def test_split_lists_match_unsplit_and_oracle(gsr_mod, cfg):
         s = sg.street(rng, 60_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
         se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
     a, _ = _render(s, se, opts=dict(split_len=2 ** 31 - 1))
-    b, _ = _render(s, se, opts=dict(split_len=16))
+    b, _ = _render(s, se, opts=dict(split_len=split))   # 160, 480: checkpointed re-walks
     assert np.abs(a - b).max() < 2e-5 * max(1.0, np.abs(a).max())
     rays = np.arange(se.width * se.height)
     ref, fl, _ = oracle.render(s, se, rays)
