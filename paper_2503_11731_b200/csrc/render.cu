@@ -574,14 +574,14 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t len, uint32_t L) {
     return b >= NB ? NB - 1 : b;
 }
 
-// Segment length: fixed (opts split_len > 0), else adaptive -- an eighth of
-// a fair share of the frame's pairs per resident CTA (at least LMIN), so the
-// longest-first schedule keeps every SM busy to the end and the exact-stop
-// re-walk of one segment stays short (measured best on the Chunked forward
-// camera, tools/sweep.py).
+// Segment length: fixed (opts split_len > 0), else adaptive -- a quarter of a
+// fair share of the frame's pairs per resident CTA (at least LMIN), so the
+// longest-first schedule keeps every SM busy to the end while the exact-stop
+// re-walk (one checkpoint interval) stays short (measured on the Chunked
+// forward camera, fisheye and LiDAR frames with tools/sweep.py).
 __device__ __forceinline__ uint32_t seg_len(const SchedHdr *h, uint32_t lfix, uint32_t ctas) {
     if (lfix) return lfix;
-    const uint32_t share = (h->P / (8u * ctas) + 255u) & ~255u;
+    const uint32_t share = (h->P / (4u * ctas) + 255u) & ~255u;
     return share > LMIN ? share : LMIN;
 }
 
