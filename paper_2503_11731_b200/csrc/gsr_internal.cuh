@@ -55,7 +55,9 @@ enum : int {
 };
 // PH_BBX / PH_BBY (and FE_, LI_ alike): conservative pixel bounding box of the
 // surfel's support, inclusive, as two packed u16 pairs (lo | hi << 16); for
-// LiDAR the column range may run past width-1 (azimuth wrap).
+// LiDAR the column range may run past width-1 (azimuth wrap).  Pinhole: the
+// box of the 3-sigma disk alone (empty: lo = 0xffff, hi = 0); the low-pass
+// disc is the circle of radius^2 PH_RCUT2 about the centre.
 // Fisheye / LiDAR (ray direction d = m + e, m = unit centre direction,
 // stored hi+lo): u = U.e / D, v = V.e / D, range t = rdet / D, D = det + N.e.
 enum : int {

@@ -491,6 +491,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
     vis = vis && (su > 0.f) && (sv > 0.f) && isfinite(su) && isfinite(sv);
     int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
     int pb[4] = {0, 0, -1, -1};   // conservative pixel bbox (x0,y0,x1,y1), inclusive
+    int cpb[4] = {0xffff, 0xffff, 0, 0};   // pinhole: pixel bbox of the 3-sigma disk only
     double A[3], Bv[3], N[3];
     if (vis) {
         const float4 qf = __ldg(reinterpret_cast<const float4 *>(s.quats) + i);
@@ -518,6 +519,13 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             Box bx;
             bx.init();
             pinhole_disk_bound(se, (double)op.near_plane, mu, a, b, bx);
+            {   // pixel box of the 3-sigma disk alone (the record's box; the low-pass disc is
+                // tested from the centre and radius by the compositor); empty: x0 = y0 = 0xffff
+                int ttx0, tty0, ttx1, tty1, cb[4];
+                if (box_to_tiles(bx, se.width, se.height, se.tw, se.th, ttx0, tty0, ttx1, tty1, cb)) {
+                    for (int k = 0; k < 4; ++k) cpb[k] = cb[k];
+                }
+            }
             const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
             const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
             bx.add(cx - rlp, cy - rlp);
@@ -677,8 +685,8 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         sh_colour(s.sh + (size_t)i * nc * 3, s.sh_degree, vx * vn, vy * vn, vz * vn, rgb);
         R[PH_R] = rgb[0]; R[PH_G] = rgb[1]; R[PH_B] = rgb[2];
         R[PH_NX] = nsx; R[PH_NY] = nsy; R[PH_NZ] = nsz;
-        R[PH_BBX] = pack_bb(pb[0], pb[2]);
-        R[PH_BBY] = pack_bb(pb[1], pb[3]);
+        R[PH_BBX] = pack_bb(cpb[0], cpb[2]);
+        R[PH_BBY] = pack_bb(cpb[1], cpb[3]);
         float4 *dst = reinterpret_cast<float4 *>(rec + (size_t)i * PH_FLOATS);
 #pragma unroll
         for (int k = 0; k < PH_FLOATS / 4; ++k)

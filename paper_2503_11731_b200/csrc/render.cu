@@ -200,15 +200,38 @@ __device__ __forceinline__ bool box_hits(uint32_t bx, uint32_t by, const SubTile
     return okx && y0 <= st.y1 && y1 >= st.y0;
 }
 
+// Can the record contribute to any sample of the sub-tile?  Pinhole: the
+// 3-sigma disk's pixel box or the low-pass disc (circle about the projected
+// centre, radius^2 = RCUT2, widened by 1e-3 px for the fp32 centre) reaches a
+// pixel centre of the sub-tile.  Others: the pixel box.
+template <int KIND>
+__device__ __forceinline__ bool rec_hits(const float4 *__restrict__ r, const SubTile &st, int W) {
+    constexpr int BB4 = Rec<KIND>::BB / 4;
+    const float4 bb = r[BB4];
+    if (box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, W)) return true;
+    if (KIND != GS_PINHOLE) return false;
+    const float4 c = r[2];
+    const float cx = c.x + c.z, cy = c.y + c.w, r2 = r[3].x;
+    const float ddx = fmaxf(fmaxf((float)st.x0 + 0.5f - cx, cx - ((float)st.x1 + 0.5f)), 0.f);
+    const float ddy = fmaxf(fmaxf((float)st.y0 + 0.5f - cy, cy - ((float)st.y1 + 0.5f)), 0.f);
+    return fmaf(ddx, ddx, ddy * ddy) <= fmaf(r2, 1.0001f, 1e-3f);
+}
+
 // One (sample, surfel) evaluation in list order.  Returns false once the ray
 // stops (the surfel that would push T below t_min is not composited, R3).
 template <int KIND, bool STATS>
 __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const Ray &ry, const DevOpts &op,
                                             Acc &a, uint32_t &n_eval, uint32_t &n_comp) {
-    if (STATS) {
+    if (STATS) {   // the sample lies in the record's conservative support region
         constexpr int BB4 = Rec<KIND>::BB / 4;
         const float4 bb = r[BB4];
-        if (in_box(__float_as_uint(bb.z), __float_as_uint(bb.w), ry.pxi, ry.pxw, ry.pyi)) ++n_eval;
+        bool in = in_box(__float_as_uint(bb.z), __float_as_uint(bb.w), ry.pxi, ry.pxw, ry.pyi);
+        if (KIND == GS_PINHOLE && !in) {
+            const float4 c = r[2];
+            const float ex = ry.px - (c.x + c.z), ey = ry.py - (c.y + c.w);
+            in = fmaf(ex, ex, ey * ey) <= r[3].x;
+        }
+        if (in) ++n_eval;
     }
     float rho, dep, o;
     if (KIND == GS_PINHOLE) {
@@ -446,11 +469,7 @@ __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const 
             const int cnt = *(volatile uint32_t *)&pp.stop_seq[slot] == gg ? -1 : (int)min(32u, e - (s + b * 32));
             if (cnt >= 0 && !wdone) {
                 const float4 *buf = ring + slot * 32 * S4;
-                bool hit = false;
-                if (lane < cnt) {
-                    const float4 bb = buf[lane * S4 + BB4];
-                    hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
-                }
+                const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, st, se.width);
                 const uint32_t bits = __ballot_sync(FULL, hit);
                 if (bits && !done) {
                     eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
@@ -505,11 +524,7 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
         __syncwarp();
         const float4 *buf = buf2 + (b & 1) * 32 * S4;
         const int cnt = (int)min(32u, e - (s + b * 32));
-        bool hit = false;
-        if (lane < cnt) {
-            const float4 bb = buf[lane * S4 + BB4];
-            hit = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, se.width);
-        }
+        const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, st, se.width);
         const uint32_t bits = __ballot_sync(FULL, hit);
         if (bits && !done) {
             eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
