@@ -659,10 +659,10 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 // segment).  Unsplit tiles are written out; segments of split tiles leave
 // their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
-__global__ void __maxnreg__(64) k_render(
+__device__ __forceinline__ void render_body(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
-    const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
+    const DevSensor &se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
@@ -716,6 +716,31 @@ __global__ void __maxnreg__(64) k_render(
             p[8 * npix] = a.n2; p[9 * npix] = __uint_as_float(stopped ? stop_b + 1u : 0u);   // 0 = no local stop
         }
     }
+}
+
+// Register budgets per sensor kind (measured): pinhole compositing runs best
+// at 56 registers per thread (seven 5-warp CTAs per SM), fisheye and LiDAR at
+// 64 (fewer spills).
+template <bool STATS>
+__global__ void __maxnreg__(56) k_render_pinhole(
+    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
+    const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
+    const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
+    float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
+    render_body<GS_PINHOLE, STATS>(rec, values, ranges, d_overflow, se, op, h, items, split_base, partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
+}
+
+template <int KIND, bool STATS>
+__global__ void __maxnreg__(64) k_render(
+    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
+    const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
+    const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
+    float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
+    float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
+    render_body<KIND, STATS>(rec, values, ranges, d_overflow, se, op, h, items, split_base, partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
 }
 
 // ---------------------------------------------------------------- merge of split lists
@@ -896,12 +921,13 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const bool piped = npix > 32;   // multi-warp tiles: a producer warp + the staging ring
     const size_t sm = (size_t)(piped ? KSLOTS : 2) * 32 * Rec<KIND>::S4 * 16;
     const int nthr = piped ? npix + 32 : npix;
-    e = cudaFuncSetAttribute(k_render<KIND, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    auto *kern = KIND == GS_PINHOLE ? k_render_pinhole<STATS> : k_render<KIND, STATS>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_render<KIND, STATS>, nthr, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nthr, sm);
     const unsigned ctas = (unsigned)std::max(1, nsm * std::max(per, 1));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)W.max_items));
     const unsigned gt = (unsigned)((ntiles + 255) / 256);
@@ -914,7 +940,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
-    k_render<KIND, STATS><<<grid, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
+    kern<<<grid, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
                                                   items, split_base, partials, ckpt, o0, o1, o2, o3, stats, lfix,
                                                   ctas);
     e = cudaGetLastError();
