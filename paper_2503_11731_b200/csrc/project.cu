@@ -48,8 +48,9 @@ __device__ __forceinline__ void fisheye_project(const DevSensor &se, const doubl
     const double th = atan2(rxy, m[2]);
     const double td = kb_theta_d(se, th);
     if (rxy > 0.0) {
-        px = (double)se.cx + (double)se.fx * td * m[0] / rxy;
-        py = (double)se.cy + (double)se.fy * td * m[1] / rxy;
+        const double q = td / rxy;
+        px = (double)se.cx + (double)se.fx * q * m[0];
+        py = (double)se.cy + (double)se.fy * q * m[1];
     } else {
         px = se.cx;
         py = se.cy;
@@ -526,14 +527,15 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                     for (int k = 0; k < 4; ++k) cpb[k] = cb[k];
                 }
             }
-            const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
-            const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
+            const double iz = 1.0 / mu[2];
+            const double cx = (double)se.fx * mu[0] * iz + (double)se.cx;
+            const double cy = (double)se.fy * mu[1] * iz + (double)se.cy;
             bx.add(cx - rlp, cy - rlp);
             bx.add(cx + rlp, cy + rlp);
             vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1, pb);
         } else {
-            const double r = sqrt(dot3(mu, mu));
-            const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
+            const double r = sqrt(dot3(mu, mu)), ir = 1.0 / r;
+            const double m[3] = {mu[0] * ir, mu[1] * ir, mu[2] * ir};
             const double R3 = Rr * (double)fmaxf(su, sv);
             const bool whole = !(R3 < 0.999 * r);
             // angular box of the support disk (elevation above the sensor xy
@@ -595,9 +597,10 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                     vis = beam_rows(se, ab.s_lo - eps, ab.s_hi + eps, r0, r1);
                     allaz = ab.all_az;
                     if (!allaz) {
-                        const double step = (double)se.az_step;
-                        const double ulo = (ab.azc + ab.daz_lo - (double)se.az0) / step;
-                        const double uhi = (ab.azc + ab.daz_hi - (double)se.az0) / step;
+                        // column bounds widened by one column below: a reciprocal step is exact enough
+                        const double step = (double)se.az_step, istep = 1.0 / step;
+                        const double ulo = (ab.azc + ab.daz_lo - (double)se.az0) * istep;
+                        const double uhi = (ab.azc + ab.daz_hi - (double)se.az0) * istep;
                         double jlo = ceil(ulo) - 1.0, jhi = floor(uhi) + 1.0;
                         if (se.full_turn) {
                             if (jhi - jlo + 1.0 >= (double)W) {
@@ -662,15 +665,17 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         cross3(mu, A, r1);    // (mu x t_u) / s_v
         const double det = dot3(N, mu);
         const double ifx = 1.0 / (double)se.fx, ify = 1.0 / (double)se.fy;
-        R[PH_A00] = (float)(r0[0] / su * ifx);
-        R[PH_A01] = (float)(r0[1] / su * ify);
-        R[PH_A10] = (float)(r1[0] / sv * ifx);
-        R[PH_A11] = (float)(r1[1] / sv * ify);
+        const double isu = 1.0 / (double)su, isv = 1.0 / (double)sv;
+        R[PH_A00] = (float)(r0[0] * isu * ifx);
+        R[PH_A01] = (float)(r0[1] * isu * ify);
+        R[PH_A10] = (float)(r1[0] * isv * ifx);
+        R[PH_A11] = (float)(r1[1] * isv * ify);
         R[PH_A20] = (float)(N[0] * ifx);
         R[PH_A21] = (float)(N[1] * ify);
-        R[PH_QC] = (float)(det / mu[2]);
-        const double cx = (double)se.fx * mu[0] / mu[2] + (double)se.cx;
-        const double cy = (double)se.fy * mu[1] / mu[2] + (double)se.cy;
+        const double iz = 1.0 / mu[2];
+        R[PH_QC] = (float)(det * iz);
+        const double cx = (double)se.fx * mu[0] * iz + (double)se.cx;
+        const double cy = (double)se.fy * mu[1] * iz + (double)se.cy;
         R[PH_RCUT3] = rcut3;
         split_hilo(cx, R[PH_CHX], R[PH_CLX]);
         split_hilo(cy, R[PH_CHY], R[PH_CLY]);
@@ -696,16 +701,17 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         float R[NF];
 #pragma unroll
         for (int k = 0; k < NF; ++k) R[k] = 0.f;
-        const double r = sqrt(dot3(mu, mu));
-        const double m[3] = {mu[0] / r, mu[1] / r, mu[2] / r};
+        const double r = sqrt(dot3(mu, mu)), ir = 1.0 / r;
+        const double m[3] = {mu[0] * ir, mu[1] * ir, mu[2] * ir};
         for (int k = 0; k < 3; ++k) split_hilo(m[k], R[RY_MH + k], R[RY_ML + k]);
         double u[3], v[3];
         cross3(Bv, m, u);   // U = r (R t_v x m) / s_u
         cross3(m, A, v);    // V = r (m x R t_u) / s_v
         const double det = dot3(N, m);
+        const double rsu = r / (double)su, rsv = r / (double)sv;
         for (int k = 0; k < 3; ++k) {
-            R[RY_U + k] = (float)(r * u[k] / su);
-            R[RY_V + k] = (float)(r * v[k] / sv);
+            R[RY_U + k] = (float)(rsu * u[k]);
+            R[RY_V + k] = (float)(rsv * v[k]);
             R[RY_N + k] = (float)N[k];
         }
         R[RY_DET] = (float)det;
@@ -731,7 +737,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         } else {
             R[LI_INT] = s.inten ? __ldg(s.inten + i) : 0.f;
             const float lg = s.drop ? __ldg(s.drop + i) : 0.f;
-            R[LI_DROP] = (float)(1.0 / (1.0 + exp(-(double)lg)));
+            R[LI_DROP] = 1.f / (1.f + expf(-lg));   // fp32 sigmoid: error ~1e-7, far inside the 1e-4 tolerance
             R[LI_BBX] = pack_bb(pb[0], pb[2]);
             R[LI_BBY] = pack_bb(pb[1], pb[3]);
         }
@@ -743,8 +749,14 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
 }
 
 // One thread per candidate (grid-stride over the compacted list of k_cull).
+#ifndef PROJ_MINB_CAM
+#define PROJ_MINB_CAM 3
+#endif
+#ifndef PROJ_MINB_LIDAR
+#define PROJ_MINB_LIDAR 4
+#endif
 template <int KIND>
-__global__ void __launch_bounds__(256, 3) k_project(DevSurfels s, const __grid_constant__ DevSensor se, DevOpts op,
+__global__ void __launch_bounds__(256, KIND == GS_LIDAR_SPINNING ? PROJ_MINB_LIDAR : PROJ_MINB_CAM) k_project(DevSurfels s, const __grid_constant__ DevSensor se, DevOpts op,
                                                  const uint32_t *__restrict__ cand, const ProjHeader *hdr,
                                                  float *__restrict__ rec, short4 *__restrict__ rect,
                                                  uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
@@ -842,7 +854,19 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * 8);
+    // grid-stride k_project: exactly the resident CTAs (whole waves, no tail wave)
+    static int occ[3] = {0, 0, 0};
+    if (!occ[se.kind]) {
+        int o = 0;
+        if (se.kind == GS_PINHOLE)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_PINHOLE>, 256, 0);
+        else if (se.kind == GS_FISHEYE_EQUIDISTANT)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_FISHEYE_EQUIDISTANT>, 256, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_LIDAR_SPINNING>, 256, 0);
+        occ[se.kind] = o > 0 ? o : 1;
+    }
+    const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * occ[se.kind]);
     note_launch(se.kind == GS_LIDAR_SPINNING ? 2 : 3);   // [k_cull +] k_project + k_compact
     if (se.kind == GS_PINHOLE) {
         k_cull<GS_PINHOLE><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);

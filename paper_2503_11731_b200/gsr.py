@@ -64,7 +64,9 @@ def load(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     so = _build.SO
-    if build_if_missing:
+    if os.environ.get("GSR_DEV_LIB"):   # dev sweeps only: an alternative in-tree build
+        so = os.environ["GSR_DEV_LIB"]
+    elif build_if_missing:
         so = _build.build()
     if not os.path.exists(so):
         raise ImportError(f"libgsr.so not found at {so}; run paper_2503_11731_b200/build.py")
