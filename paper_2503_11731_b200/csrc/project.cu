@@ -178,19 +178,21 @@ __device__ __forceinline__ double dot3(const double a[3], const double b[3]) {
 }
 
 // LiDAR: rows whose beam elevation sine lies in [lo, hi] (table strictly decreasing)
-__device__ __forceinline__ bool beam_rows(const DevSensor &se, double lo, double hi, int &r0, int &r1) {
+// (sb: the sensor's sine table staged in shared memory -- divergent lookups
+// into the kernel-parameter bank would serialise across the warp)
+__device__ __forceinline__ bool beam_rows(const float *sb, int nbeams, double lo, double hi, int &r0, int &r1) {
     // first row with sin(beam) <= hi
-    int a = 0, b = se.nbeams;
+    int a = 0, b = nbeams;
     while (a < b) {
         const int m = (a + b) >> 1;
-        if ((double)se.sbeam[m] <= hi) b = m; else a = m + 1;
+        if ((double)sb[m] <= hi) b = m; else a = m + 1;
     }
     r0 = a;
     // last row with sin(beam) >= lo
-    a = 0; b = se.nbeams;
+    a = 0; b = nbeams;
     while (a < b) {
         const int m = (a + b) >> 1;
-        if ((double)se.sbeam[m] < lo) b = m; else a = m + 1;
+        if ((double)sb[m] < lo) b = m; else a = m + 1;
     }
     r1 = a - 1;
     return r0 <= r1;
@@ -208,9 +210,13 @@ struct AngBox {
 // Range of the linear-fractional f(c,s) = (n0 + n1 c + n2 s)/(d0 + d1 c + d2 s)
 // over the unit disk (denominator > 0 on it): the extremes lie on the circle
 // at the two roots of A c + B s + C = 0.
+// fp32 instantiation: fast division (2 ulp; its callers' margins are ~10x wider)
+__device__ __forceinline__ double lf_div(double a, double b) { return a / b; }
+__device__ __forceinline__ float lf_div(float a, float b) { return __fdividef(a, b); }
+
 template <typename T>
 __device__ void lf_range(T n0, T n1, T n2, T d0, T d1, T d2, T &lo, T &hi) {
-    lo = hi = n0 / d0;
+    lo = hi = lf_div(n0, d0);
     const T A = n2 * d0 - n0 * d2, B = n0 * d1 - n1 * d0, C = n2 * d1 - n1 * d2;
     const T rr = A * A + B * B;
     if (rr > T(0)) {
@@ -219,14 +225,14 @@ __device__ void lf_range(T n0, T n1, T n2, T d0, T d1, T d2, T &lo, T &hi) {
         const T cs[2][2] = {{(-A * C + B * q) * irr, (-B * C - A * q) * irr},
                             {(-A * C - B * q) * irr, (-B * C + A * q) * irr}};
         for (int k = 0; k < 2; ++k) {
-            const T f = (n0 + n1 * cs[k][0] + n2 * cs[k][1]) / (d0 + d1 * cs[k][0] + d2 * cs[k][1]);
+            const T f = lf_div(n0 + n1 * cs[k][0] + n2 * cs[k][1], d0 + d1 * cs[k][0] + d2 * cs[k][1]);
             lo = fmin(lo, f);
             hi = fmax(hi, f);
         }
     }
     for (int k = 0; k < 4; ++k) {   // safety points on the circle
         const T c = k == 0 ? T(1) : (k == 1 ? T(-1) : T(0)), s = k == 2 ? T(1) : (k == 3 ? T(-1) : T(0));
-        const T f = (n0 + n1 * c + n2 * s) / (d0 + d1 * c + d2 * s);
+        const T f = lf_div(n0 + n1 * c + n2 * s, d0 + d1 * c + d2 * s);
         lo = fmin(lo, f);
         hi = fmax(hi, f);
     }
@@ -462,7 +468,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
 template <int KIND>
 __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op,
                                             int64_t i, float *__restrict__ rec, short4 *__restrict__ rect,
-                                            uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
+                                            uint32_t *__restrict__ keys, uint32_t *__restrict__ counts,
+                                            const float *sb) {
     if (KIND != GS_LIDAR_SPINNING && s.sh) {   // the SH block is read last: start it towards L2 now
         const int nc3 = (s.sh_degree + 1) * (s.sh_degree + 1) * 3;
         const char *p = reinterpret_cast<const char *>(s.sh + (size_t)i * nc3);
@@ -484,7 +491,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
     const float o = __ldg(s.opac + i);
     // opacity-aware support: alpha >= alpha_min needs rho <= 2 ln(o / alpha_min)
     float rc = op.support;
-    if (op.alpha_min > 0.f) rc = fminf(rc, 2.0f * logf(o / op.alpha_min));
+    if (op.alpha_min > 0.f) rc = fminf(rc, 2.0f * logf(__fdividef(o, op.alpha_min)));   // +1e-4 margin below
     const float rcut3 = rc * 1.0001f + 1e-4f;
     bool vis = (keyf >= op.near_plane) && (rcut3 >= 0.f) && (o > 0.f);
 
@@ -594,7 +601,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                 bool allaz = whole;
                 if (!whole) {
                     const double eps = 2e-6;   // sine units; covers the fp32 sine table
-                    vis = beam_rows(se, ab.s_lo - eps, ab.s_hi + eps, r0, r1);
+                    vis = beam_rows(sb, se.nbeams, ab.s_lo - eps, ab.s_hi + eps, r0, r1);
                     allaz = ab.all_az;
                     if (!allaz) {
                         // column bounds widened by one column below: a reciprocal step is exact enough
@@ -606,9 +613,12 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                             if (jhi - jlo + 1.0 >= (double)W) {
                                 allaz = true;
                             } else {
-                                double k = floor(jlo / (double)W);
+                                // wrap jlo into [0, W) (integers in fp64: exact after the fix-up)
+                                const double k = floor(jlo * (1.0 / (double)W));
                                 jlo -= k * W;
                                 jhi -= k * W;
+                                if (jlo >= (double)W) { jlo -= W; jhi -= W; }
+                                if (jlo < 0.0) { jlo += W; jhi += W; }
                                 c0 = (int)jlo;
                                 c1 = (int)jhi;   // may exceed W-1: wraps
                             }
@@ -760,9 +770,14 @@ __global__ void __launch_bounds__(256, KIND == GS_LIDAR_SPINNING ? PROJ_MINB_LID
                                                  const uint32_t *__restrict__ cand, const ProjHeader *hdr,
                                                  float *__restrict__ rec, short4 *__restrict__ rect,
                                                  uint32_t *__restrict__ keys, uint32_t *__restrict__ counts) {
+    __shared__ float sb[KIND == GS_LIDAR_SPINNING ? GS_MAX_BEAMS : 1];
+    if (KIND == GS_LIDAR_SPINNING) {
+        for (int k = threadIdx.x; k < se.nbeams; k += blockDim.x) sb[k] = se.sbeam[k];
+        __syncthreads();
+    }
     const uint32_t nc = cand ? hdr->n_cand : (uint32_t)s.n;   // no cand list: every surfel
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
-        project_one<KIND>(s, se, op, cand ? (int64_t)cand[c] : (int64_t)c, rec, rect, keys, counts);
+        project_one<KIND>(s, se, op, cand ? (int64_t)cand[c] : (int64_t)c, rec, rect, keys, counts, sb);
 }
 
 // ------------------------------------------------------------------ compaction
