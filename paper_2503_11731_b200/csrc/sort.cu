@@ -23,10 +23,7 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // 4096
 constexpr int RS_BINS = 256;
-#ifndef RS_LB_N
-#define RS_LB_N 8
-#endif
-constexpr int RS_LB = RS_LB_N;        // look-back window (predecessor tiles per round trip)
+constexpr int RS_LB = 8;   // look-back window: predecessor tiles read per round trip
 constexpr uint32_t RS_AGG = 1u << 30, RS_PRE = 2u << 30, RS_VAL = (1u << 30) - 1;
 
 struct SortWs {   // workspace layout of gs_bin_sort
@@ -118,13 +115,7 @@ __global__ void k_hist_scan(uint32_t *ghist, int npass, const int32_t *d_overflo
 }
 
 // ------------------------------------------------------------------ onesweep pass
-// PACK (keys < 2^16, the tile passes): the in-warp rank rides in the key's
-// upper half, which frees 16 registers per thread for a 4th CTA per SM.
-#ifndef ONESWEEP_PACK
-#define ONESWEEP_PACK 1
-#endif
-template <bool PACK>
-__global__ void __launch_bounds__(RS_THREADS, PACK ? 4 : 3) k_onesweep(
+__global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, const uint32_t *d_n, int shift, int bits,
     const uint32_t *__restrict__ gbase, uint32_t *status, uint32_t *counter,
@@ -146,12 +137,12 @@ __global__ void __launch_bounds__(RS_THREADS, PACK ? 4 : 3) k_onesweep(
     if (t0 >= n) return;
     const uint32_t mask = (1u << bits) - 1;
     const uint32_t wbase = t0 + warp * (32 * RS_ITEMS);
-    uint32_t k[RS_ITEMS], v[RS_ITEMS], rk[PACK ? 1 : RS_ITEMS];
+    uint32_t k[RS_ITEMS], v[RS_ITEMS], rk[RS_ITEMS];
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         const uint32_t idx = wbase + j * 32 + lane;
         const bool ok = idx < n;
-        k[j] = ok ? kin[idx] : (PACK ? 0xffffu : 0xffffffffu);
+        k[j] = ok ? kin[idx] : 0xffffffffu;
         v[j] = ok ? vin[idx] : 0u;
     }
     // Stable in-warp ranks: for item j the peers with the same digit come from
@@ -170,9 +161,7 @@ __global__ void __launch_bounds__(RS_THREADS, PACK ? 4 : 3) k_onesweep(
         const int leader = __ffs(peers) - 1;
         uint32_t old = 0;
         if (ok && lane == leader) old = atomicAdd(&whist[warp][d], (uint32_t)__popc(peers));
-        const uint32_t r = __shfl_sync(FULL_MASK, old, leader) + __popc(peers & lt);
-        if (PACK) k[j] |= r << 16;
-        else rk[j] = r;
+        rk[j] = __shfl_sync(FULL_MASK, old, leader) + __popc(peers & lt);
     }
     __syncthreads();
     // per digit: warp-exclusive offsets and tile count
@@ -231,10 +220,9 @@ __global__ void __launch_bounds__(RS_THREADS, PACK ? 4 : 3) k_onesweep(
     for (int j = 0; j < RS_ITEMS; ++j) {
         const uint32_t idx = wbase + j * 32 + lane;
         if (idx < n) {
-            const uint32_t key = PACK ? (k[j] & 0xffffu) : k[j];
-            const uint32_t d = (key >> shift) & mask;
-            const uint32_t pos = tile_excl[d] + whist[warp][d] + (PACK ? (k[j] >> 16) : rk[j]);
-            skey[pos] = key;
+            const uint32_t d = (k[j] >> shift) & mask;
+            const uint32_t pos = tile_excl[d] + whist[warp][d] + rk[j];
+            skey[pos] = k[j];
             sval[pos] = v[j];
         }
     }
@@ -463,7 +451,7 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     const unsigned grid_d = (unsigned)(W.ntile_d > 0 ? W.ntile_d : 1);
     for (int p = 0; p < 4; ++p) {
         note_launch();
-        k_onesweep<false><<<grid_d, RS_THREADS, 0, st>>>(ki, vi, bufk[p & 1], bufv[p & 1], d_nvis, 8 * p, 8,
+        k_onesweep<<<grid_d, RS_THREADS, 0, st>>>(ki, vi, bufk[p & 1], bufv[p & 1], d_nvis, 8 * p, 8,
                                                   hist + p * RS_BINS,
                                                   (uint32_t *)(wb + W.dstat) + (size_t)p * W.ntile_d * RS_BINS,
                                                   &misc->counter[p], nullptr);
@@ -505,8 +493,7 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     for (int p = 0; p < np; ++p) {
         const int bits = min(8, tb - 8 * p);
         note_launch();
-        auto *ks = (ONESWEEP_PACK && tb <= 16) ? k_onesweep<true> : k_onesweep<false>;
-        ks<<<grid_t, RS_THREADS, 0, st>>>(tk[cur], tv[cur], tk[cur ^ 1], tv[cur ^ 1], d_np, 8 * p,
+        k_onesweep<<<grid_t, RS_THREADS, 0, st>>>(tk[cur], tv[cur], tk[cur ^ 1], tv[cur ^ 1], d_np, 8 * p,
                                                   bits, thist + p * RS_BINS,
                                                   (uint32_t *)(wb + W.tstat) + (size_t)p * W.ntile_t * RS_BINS,
                                                   &misc->counter[4 + p], d_overflow);
