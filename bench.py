@@ -255,7 +255,7 @@ def run_gsr(args):
     rank, world, device = gd.init()
     if device.type != "cuda":
         raise SystemExit("bench.py needs a CUDA device (B200)")
-    gsr.load(build_if_missing=False)   # the in-tree libgsr.so; never a fallback
+    gsr.load()   # the in-tree libgsr.so (rebuilt first if older than its sources); never a fallback
     t_gen = time.time()
     surfels_np, groups, desc = build_workload(args.workload, args.timesteps)
     n_steps_t = len(groups)
@@ -358,9 +358,11 @@ def run_gsr(args):
     t_all0 = torch.cuda.Event(enable_timing=True)
     t_all1 = torch.cuda.Event(enable_timing=True)
     t_all0.record(cur)
+    th0 = time.perf_counter()
     for _ in range(args.steps):
         step(event_log=event_log)
     t_all1.record(cur)
+    host_enqueue_ms = (time.perf_counter() - th0) * 1e3 / args.steps   # host time to enqueue a step
     torch.cuda.synchronize(device)
     gd.barrier(world, device)
     n_launch = gsr.gs_kernel_launches() - n_launch0
@@ -490,6 +492,7 @@ def run_gsr(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenegen seeds, "
                 "BASELINE.json configs; random surfels, no trained scene)", "config": desc,
                 "e2e": e2e, "gpu_launches": int(n_launch), "gpu_launches_per_step": n_launch // args.steps,
+                "host_enqueue_ms_per_step": round(host_enqueue_ms, 3),
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "stages": stage,
                 "per_config": per_config, "setup_s": {"generate": round(t_gen, 1)}}
         print(json.dumps(line), flush=True)

@@ -29,17 +29,26 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """(Re)build libgsr.so when forced or older than its sources.  Concurrent
+    callers (e.g. the ranks of a torchrun job) serialise on a lock file, and
+    the ones that wait find it fresh."""
     if not force and not _stale():
         return SO
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", SO + ".tmp"] + \
-        [os.path.join(CSRC, f) for f in SOURCES]
-    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libgsr.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
-    os.replace(SO + ".tmp", SO)
+    import fcntl
+    with open(SO + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not _stale():
+            return SO
+        tmp = f"{SO}.{os.getpid()}.tmp"
+        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + \
+            [os.path.join(CSRC, f) for f in SOURCES]
+        r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libgsr.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        os.replace(tmp, SO)
     return SO
 
 
