@@ -266,7 +266,7 @@ def run_gsr(args):
     t_gen = time.time() - t_gen
 
     surf = to_device(surfels_np, device)
-    br = BatchRenderer(surf, device=device, n_streams=args.streams)
+    br = BatchRenderer(surf, device=device, n_streams=args.streams, grid_share=args.grid_share)
     caps, contrib, evals = br.plan(my_sensors, stats=True)
     sensors = br.wrap(my_sensors)
 
@@ -483,7 +483,7 @@ def run_gsr(args):
 
     if rank == 0:
         desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
-                    if world > 1 else "1 GPU", streams=args.streams,
+                    if world > 1 else "1 GPU", streams=args.streams, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
                     l2="no flush: resident surfels (%.2f GB) and outputs (%.1f GB) exceed the 126 MB L2" % (
                         sum(v.numel() * 4 for v in surf.values() if isinstance(v, torch.Tensor)) / 1e9,
                         sum(t.numel() * 4 for t in slabs_full.values()) / 1e9))
@@ -510,7 +510,9 @@ def main():
     ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
     ap.add_argument("--workload", default="chunked", choices=["chunked", "mid", "fisheye", "lidar", "tiny"])
     ap.add_argument("--timesteps", type=int, default=64)
-    ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--grid-share", type=float, default=None,
+                    help="gs_opts.grid_share of every frame (default: BatchRenderer's 2/streams)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-frame rates")

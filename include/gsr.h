@@ -100,8 +100,9 @@ typedef struct {
                                     then 16x2, 8x4); GS_ERR_RANGE otherwise.  LiDAR:
                                     32 x 1 recommended.  Edge tiles may be partial.     */
     int32_t split_len;           /* tile lists longer than this are split into segments
-                                    composited in parallel and merged (0 = 16384;
-                                    INT32_MAX disables splitting)                        */
+                                    composited in parallel and merged (0 = adaptive: a
+                                    quarter of a resident CTA's fair share of the
+                                    frame's pairs, at least 1024; INT32_MAX disables)   */
     float near_plane;            /* 0.2 m                                               */
     float alpha_max;             /* 0.99                                                */
     float alpha_min;             /* 1/255                                               */
@@ -111,6 +112,13 @@ typedef struct {
     float bg_rgb[3];             /* 0,0,0                                               */
     float bg_range;              /* 0                                                   */
     float bg_raydrop;            /* 1                                                   */
+    float grid_share;            /* fraction in (0, 1] of the compositor's resident CTA
+                                    slots its persistent grid takes (0 = 1: the whole
+                                    GPU).  A caller compositing k frames concurrently on
+                                    k streams gives each about 2/k, so the frames'
+                                    projection and binning kernels find free SMs.
+                                    Results do not depend on it.  GS_ERR_RANGE outside
+                                    [0, 1].                                             */
 } gs_opts;
 
 void gs_default_opts(gs_opts *opts);

@@ -42,9 +42,16 @@ class FrameTimes:
 
 class BatchRenderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
-                 lidar_tile=(32, 1)):
+                 lidar_tile=(32, 1), grid_share: float | None = None):
+        """grid_share: fraction of the GPU's resident compositor CTA slots each
+        frame's persistent grid takes (gs_opts.grid_share); default 2/n_streams
+        (capped at 1), so about two frames composite at once and the other
+        streams' projection and binning kernels find free SMs."""
         self.device = torch.device(device)
-        self.lanes = [Renderer(surfels, opts, device, lidar_tile) for _ in range(max(1, n_streams))]
+        n_streams = max(1, n_streams)
+        o = gsr.gs_opts.from_buffer_copy(opts) if opts is not None else gsr.default_opts()
+        o.grid_share = float(grid_share) if grid_share is not None else min(1.0, 2.0 / n_streams)
+        self.lanes = [Renderer(surfels, o, device, lidar_tile) for _ in range(n_streams)]
         self.streams = [torch.cuda.Stream(self.device) for _ in self.lanes]
         self.n = self.lanes[0].n
         self.caps = None

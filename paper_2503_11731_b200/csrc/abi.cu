@@ -59,6 +59,7 @@ extern "C" void gs_default_opts(gs_opts *o) {
     o->bg_rgb[0] = o->bg_rgb[1] = o->bg_rgb[2] = 0.f;
     o->bg_range = 0.f;
     o->bg_raydrop = 1.f;
+    o->grid_share = 0.f;
 }
 
 extern "C" int32_t gs_record_bytes(int32_t kind) { return record_floats(kind) * 4; }
@@ -79,6 +80,7 @@ static gs_status check_opts(const gs_opts *o) {
     if (o->tile_w < 1 || o->tile_h < 1 || (int64_t)o->tile_w * o->tile_h > 512)
         return fail(GS_ERR_RANGE, "tile shape must hold 32..512 samples");
     if (o->split_len < 0) return fail(GS_ERR_RANGE, "split_len must be >= 0");
+    if (!(o->grid_share >= 0.f && o->grid_share <= 1.f)) return fail(GS_ERR_RANGE, "grid_share outside [0, 1]");
     if (!(o->near_plane > 0.f) || !(o->alpha_max > 0.f) || !(o->alpha_max <= 1.f) ||
         !(o->alpha_min >= 0.f) || !(o->t_min >= 0.f) || !(o->support_rho > 0.f) ||
         !(o->lowpass_sigma_px > 0.f))
@@ -181,6 +183,7 @@ static DevOpts make_dev_opts(const gs_opts *o) {
     for (int c = 0; c < 3; ++c) d.bg[c] = o->bg_rgb[c];
     d.bg_range = o->bg_range;
     d.bg_raydrop = o->bg_raydrop;
+    d.grid_share = o->grid_share > 0.f ? o->grid_share : 1.f;
     return d;
 }
 

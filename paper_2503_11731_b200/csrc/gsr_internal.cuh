@@ -31,6 +31,7 @@ struct DevOpts {
     float near_plane, alpha_max, alpha_min, t_min, support, sigma2, inv_sigma2;
     float bg[3];
     float bg_range, bg_raydrop;
+    float grid_share;   // host side: fraction of the compositor's resident CTA slots to launch
 };
 
 struct DevSurfels {

@@ -928,7 +928,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nthr, sm);
-    const unsigned ctas = (unsigned)std::max(1, nsm * std::max(per, 1));
+    const unsigned ctas = (unsigned)std::max(1, (int)((float)(nsm * std::max(per, 1)) * op.grid_share));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)W.max_items));
     const unsigned gt = (unsigned)((ntiles + 255) / 256);
     note_launch(4);
@@ -956,7 +956,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
         int per_rw = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_rw, k_rewalk<KIND>, nthr, sm);
         const unsigned grid_rw = (unsigned)std::max<int64_t>(
-            1, std::min<int64_t>((int64_t)nsm * std::max(per_rw, 1), (int64_t)W.max_slots));
+            1, std::min<int64_t>((int64_t)((float)(nsm * std::max(per_rw, 1)) * op.grid_share), (int64_t)W.max_slots));
         k_rewalk<KIND><<<grid_rw, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_list,
                                                   mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
         e = cudaGetLastError();

@@ -47,7 +47,8 @@ class gs_opts(C.Structure):
                 ("near_plane", C.c_float),
                 ("alpha_max", C.c_float), ("alpha_min", C.c_float), ("t_min", C.c_float),
                 ("support_rho", C.c_float), ("lowpass_sigma_px", C.c_float),
-                ("bg_rgb", C.c_float * 3), ("bg_range", C.c_float), ("bg_raydrop", C.c_float)]
+                ("bg_rgb", C.c_float * 3), ("bg_range", C.c_float), ("bg_raydrop", C.c_float),
+                ("grid_share", C.c_float)]
 
 
 EXPORTS = ["gs_default_opts", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",

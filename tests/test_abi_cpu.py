@@ -44,6 +44,17 @@ def test_default_opts_are_north_star(gsr):
     assert o.t_min == pytest.approx(1e-4) and o.support_rho == 9.0
     assert o.lowpass_sigma_px == pytest.approx(2 ** -0.5) and o.near_plane == pytest.approx(0.2)
     assert o.bg_raydrop == 1.0
+    assert o.grid_share == 0.0   # 0 = the compositor's grid fills the GPU
+
+
+@pytest.mark.parametrize("share,ok", [(0.0, True), (0.25, True), (1.0, True), (-0.1, False), (1.5, False),
+                                      (float("nan"), False)])
+def test_grid_share_validation(gsr, share, ok):
+    cam = gsr.Sensor(sg.tiny().sensors[0])
+    o = gsr.default_opts(grid_share=share)
+    assert (gsr.gs_num_tiles(cam, o) > 0) == ok
+    if not ok:
+        assert "grid_share" in gsr.load().gs_last_error().decode()
 
 
 def _call_project(gsr, sensor, opts=None, n=0):

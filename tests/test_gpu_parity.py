@@ -159,6 +159,21 @@ def test_split_lists_match_unsplit_and_oracle(gsr_mod, cfg, split):
     assert st["ok"], st
 
 
+@pytest.mark.parametrize("share", [0.05, 0.5])
+def test_grid_share_does_not_change_results(gsr_mod, share):
+    """A smaller persistent compositor grid (gs_opts.grid_share) only changes
+    the adaptive split length and the schedule: same image to fp32 rounding."""
+    c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
+    a, _ = _render(c.surfels, c.sensors[0])
+    b, _ = _render(c.surfels, c.sensors[0], opts=dict(grid_share=share))
+    assert np.abs(a - b).max() < 2e-5 * max(1.0, np.abs(a).max())
+    li = sg.street(np.random.default_rng(5), 60_000, -60.0, 60.0, 0, lidar_attrs=True, with_sh=False)
+    se = sg.lidar64(sg.lidar_pose([0, 1.8, 0]), height=32, width=360)
+    a, _ = _render(li, se)
+    b, _ = _render(li, se, opts=dict(grid_share=share))
+    assert np.abs(a - b).max() < 2e-5 * max(1.0, np.abs(a).max())
+
+
 def test_deterministic_repeat(gsr_mod):
     c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
     a, _ = _render(c.surfels, c.sensors[0])
