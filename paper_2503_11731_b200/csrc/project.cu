@@ -357,7 +357,7 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
 // (decoupled look-back); the others get the culled outputs here.
 template <int KIND>
 __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op, int64_t i,
-                                         uint32_t &keybits) {
+                                         uint32_t &keybits, const float *sb) {
     const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1), mz = __ldg(s.means + 3 * i + 2);
     float keyf;
     if (KIND == GS_PINHOLE) {
@@ -392,14 +392,41 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
     }
     const float r = sqrtf(X * X + Y * Y + Z * Z);
     if (!(r > R * 1.01f)) return true;
-    const float beta = asinf(R / r);
     if (KIND == GS_FISHEYE_EQUIDISTANT) {
+        const float beta = asinf(R / r);
         const float th = acosf(fminf(1.f, fmaxf(-1.f, Z / r)));
         return th - beta <= se.theta_max + 0.15f;
     }
-    const float el = asinf(fminf(1.f, fmaxf(-1.f, Z / r)));
-    const float top = se.beam[0], bot = se.beam[se.nbeams - 1];
-    return el + beta >= bot - 1e-4f && el - beta <= top + 1e-4f;
+    // LiDAR: elevation range of the support disk itself (a ground surfel seen at a
+    // grazing angle is thin in elevation and usually falls between two beams).
+    // Disk z-extent: mu_z +- Rr sqrt((s_u t_u,z)^2 + (s_v t_v,z)^2) (t_u, t_v in the
+    // sensor frame); horizontal distance within rho_c +- Rr max(s_u, s_v); sines of
+    // the extreme elevations from those, widened by 1e-4 (fp32 here); then some
+    // beam's sine must lie in the range.
+    const float4 q = __ldg(reinterpret_cast<const float4 *>(s.quats) + i);
+    const float inq = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    const float qw = q.x * inq, qx = q.y * inq, qy = q.z * inq, qz = q.w * inq;
+    // world t_u, t_v = first two columns of the rotation; their sensor-frame z = row 2 of R_s times them
+    const float tu0 = 1.f - 2.f * (qy * qy + qz * qz), tu1 = 2.f * (qx * qy + qw * qz), tu2 = 2.f * (qx * qz - qw * qy);
+    const float tv0 = 2.f * (qx * qy - qw * qz), tv1 = 1.f - 2.f * (qx * qx + qz * qz), tv2 = 2.f * (qy * qz + qw * qx);
+    const float az = se.R[6] * tu0 + se.R[7] * tu1 + se.R[8] * tu2;
+    const float bz = se.R[6] * tv0 + se.R[7] * tv1 + se.R[8] * tv2;
+    const float Rr = R / fmaxf(sc.x, sc.y);   // 1.001 sqrt(rcut) (+ the absolute margin, scaled)
+    const float mg = 1e-4f * (1.f + r);
+    const float hz = Rr * sqrtf((sc.x * az) * (sc.x * az) + (sc.y * bz) * (sc.y * bz)) + mg;
+    const float rxy = sqrtf(X * X + Y * Y);
+    const float rlo = rxy - R - mg, rhi = rxy + R + mg;
+    if (!(rlo > 1e-3f * r)) return true;   // near the vertical axis: keep
+    const float zlo = Z - hz, zhi = Z + hz;
+    const float shi = zhi >= 0.f ? zhi * rsqrtf(zhi * zhi + rlo * rlo) : zhi * rsqrtf(zhi * zhi + rhi * rhi);
+    const float slo = zlo >= 0.f ? zlo * rsqrtf(zlo * zlo + rhi * rhi) : zlo * rsqrtf(zlo * zlo + rlo * rlo);
+    const float sh = shi + 1e-4f, sl = slo - 1e-4f;
+    int lo = 0, hi = se.nbeams;   // first row with sin(beam) <= sh (table decreasing)
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (sb[m] <= sh) hi = m; else lo = m + 1;
+    }
+    return lo < se.nbeams && sb[lo] >= sl;
 }
 
 template <int KIND>
@@ -410,7 +437,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
                                                        ProjHeader *hdr) {
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_excl;
+    __shared__ float sb[KIND == GS_LIDAR_SPINNING ? GS_MAX_BEAMS : 1];   // beam sines (LiDAR)
     if (threadIdx.x == 0) s_tile = atomicAdd(&hdr->cull_counter, 1u);
+    if (KIND == GS_LIDAR_SPINNING)
+        for (int k = threadIdx.x; k < se.nbeams; k += SCAN_THREADS) sb[k] = se.sbeam[k];
     __syncthreads();
     const uint32_t tile = s_tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -422,7 +452,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
         const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
         if (i < s.n) {
             uint32_t kb;
-            const bool c = cull_one<KIND>(s, se, op, i, kb);
+            const bool c = cull_one<KIND>(s, se, op, i, kb, sb);
             if (c) { flags |= 1u << j; ++cnt; }
             // every surfel gets the culled outputs here (full, coalesced lines);
             // k_project overwrites those of the candidates it finds visible
@@ -882,7 +912,7 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
         occ[se.kind] = o > 0 ? o : 1;
     }
     const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * occ[se.kind]);
-    note_launch(se.kind == GS_LIDAR_SPINNING ? 2 : 3);   // [k_cull +] k_project + k_compact
+    note_launch(3);   // k_cull + k_project + k_compact
     if (se.kind == GS_PINHOLE) {
         k_cull<GS_PINHOLE><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_PINHOLE><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
@@ -890,9 +920,7 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
         k_cull<GS_FISHEYE_EQUIDISTANT><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_FISHEYE_EQUIDISTANT><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
     } else {
-        // a spinning LiDAR sees all around: the conservative cull passes nearly every
-        // surfel, so skip it and project every surfel in index order (coalesced)
-        cand = nullptr;
+        k_cull<GS_LIDAR_SPINNING><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_LIDAR_SPINNING><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
     }
     e = cudaGetLastError();
