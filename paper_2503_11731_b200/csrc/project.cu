@@ -350,10 +350,12 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
 // k_project) or when the sphere of radius 3.001 max(s_u, s_v) around its
 // sensor-frame centre (which holds the 3-sigma support disk) lies outside
 // the sensor's field of view widened by a margin (pinhole: 4 px beyond the
-// image, covering the low-pass disc; fisheye: 0.15 rad beyond theta_max;
-// LiDAR: 1e-4 rad beyond the beam fan).  fp32 arithmetic with margins well
-// above its error; only used to skip work -- k_project takes every decision
-// for the surfels that pass.  Passing surfels are compacted in index order
+// image, covering the low-pass disc; fisheye: 0.15 rad beyond theta_max), or
+// (LiDAR) when no beam's elevation lies in the elevation range of the support
+// disk, bounded from its exact z-extent and horizontal distance range (+1e-4
+// in sine).  fp32 arithmetic with margins well above its error; a culled
+// surfel provably meets no sample ray, so this only skips work -- k_project
+// takes every decision for the surfels that pass.  Passing surfels are compacted in index order
 // (decoupled look-back); the others get the culled outputs here.
 template <int KIND>
 __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op, int64_t i,
