@@ -125,6 +125,23 @@ struct SubTile {
     int x0, y0, x1, y1;   // inclusive
 };
 
+// Bounding rectangle of the warp's samples whose rays are still running: the
+// warp-level record test shrinks to it as samples stop (a record that only
+// covers stopped samples is skipped).  Not called when every lane is done.
+// Cameras only: LiDAR sub-tiles are one beam row whose rays stop in no
+// particular column order, and the recomputation cost more than it saved
+// there (tools/sweep.py).
+template <int KIND>
+constexpr bool ACTIVE_RECT = KIND != GS_LIDAR_SPINNING;
+__device__ __forceinline__ SubTile active_rect(const Ray &ry, bool done) {
+    SubTile a;
+    a.x0 = __reduce_min_sync(0xffffffffu, done ? 0x7fffffff : ry.pxi);
+    a.x1 = __reduce_max_sync(0xffffffffu, done ? (int)0x80000000 : ry.pxi);
+    a.y0 = __reduce_min_sync(0xffffffffu, done ? 0x7fffffff : ry.pyi);
+    a.y1 = __reduce_max_sync(0xffffffffu, done ? (int)0x80000000 : ry.pyi);
+    return a;
+}
+
 __device__ __forceinline__ SubTile sub_tile(const DevSensor &se, int tile, int warp) {
     const int tyi = tile / se.ntx, txi = tile - tyi * se.ntx;
     const int nsx = se.tw / se.sw;
@@ -204,14 +221,60 @@ __device__ __forceinline__ bool box_hits(uint32_t bx, uint32_t by, const SubTile
 // 3-sigma disk's pixel box or the low-pass disc (circle about the projected
 // centre, radius^2 = RCUT2, widened by 1e-3 px for the fp32 centre) reaches a
 // pixel centre of the sub-tile.  Others: the pixel box.
+constexpr int ELL_MIN = 4;   // boxes spanning <= this many px (width + height) skip the ellipse test
+// Pinhole: can the 3-sigma region {Q <= 0} reach the sub-tile's pixel-centre
+// rectangle?  Q(d) = |A01 d|^2 - R (a2.d + qc)^2 (d = pixel - centre) is the
+// compositor's own support test; when its quadratic part is well-conditioned
+// positive definite (a bounded ellipse) the minimum of Q over the rectangle
+// is at the ellipse centre if that lies inside, else on an edge at the
+// clamped vertex of a 1-D quadratic.  The rectangle is widened by 0.01 px and
+// the threshold by 2e-3 R w_max^2 (fp32 slack); otherwise "yes".
+__device__ __forceinline__ bool ellipse_hits(const float4 *__restrict__ r, float cx, float cy, const SubTile &st) {
+    const float4 g0 = r[0], g1 = r[1];
+    const float R = g1.w, qc = g1.z;
+    const float M00 = fmaf(g0.x, g0.x, fmaf(g0.z, g0.z, -R * g1.x * g1.x));
+    const float M11 = fmaf(g0.y, g0.y, fmaf(g0.w, g0.w, -R * g1.y * g1.y));
+    const float M01 = fmaf(g0.x, g0.y, fmaf(g0.z, g0.w, -R * g1.x * g1.y));
+    const float det = fmaf(M00, M11, -M01 * M01);
+    // well-conditioned only: no cancellation in M00, M11 or det beyond 1e-3 of their terms
+    const float t00 = fmaf(g0.x, g0.x, fmaf(g0.z, g0.z, R * g1.x * g1.x));
+    const float t11 = fmaf(g0.y, g0.y, fmaf(g0.w, g0.w, R * g1.y * g1.y));
+    if (!(M00 > 1e-3f * t00) || !(M11 > 1e-3f * t11) || !(det > 1e-3f * M00 * M11)) return true;
+    const float B0 = -R * qc * g1.x, B1 = -R * qc * g1.y, C = -R * qc * qc;
+    const float X0 = (float)st.x0 + 0.49f - cx, X1 = (float)st.x1 + 0.51f - cx;
+    const float Y0 = (float)st.y0 + 0.49f - cy, Y1 = (float)st.y1 + 0.51f - cy;
+    const float idet = 1.f / det;
+    const float sx = (M01 * B1 - M11 * B0) * idet, sy = (M01 * B0 - M00 * B1) * idet;
+    if (sx >= X0 && sx <= X1 && sy >= Y0 && sy <= Y1) return true;
+    // slack 2e-3 R w_max^2, w_max bounding |a2.d + qc| over the rectangle (Q's terms there)
+    const float wmax = fabsf(qc) + fabsf(g1.x) * fmaxf(fabsf(X0), fabsf(X1)) + fabsf(g1.y) * fmaxf(fabsf(Y0), fabsf(Y1));
+    const float tol = 2e-3f * R * wmax * wmax;
+    auto q = [&](float x, float y) {
+        return fmaf(x, fmaf(M00, x, 2.f * fmaf(M01, y, B0)), fmaf(y, fmaf(M11, y, 2.f * B1), C));
+    };
+    const float i00 = 1.f / M00, i11 = 1.f / M11;
+    const float xa = fminf(fmaxf(-(M01 * Y0 + B0) * i00, X0), X1);
+    const float xb = fminf(fmaxf(-(M01 * Y1 + B0) * i00, X0), X1);
+    const float ya = fminf(fmaxf(-(M01 * X0 + B1) * i11, Y0), Y1);
+    const float yb = fminf(fmaxf(-(M01 * X1 + B1) * i11, Y0), Y1);
+    const float m = fminf(fminf(q(xa, Y0), q(xb, Y1)), fminf(q(X0, ya), q(X1, yb)));
+    return m <= tol;
+}
+
 template <int KIND>
 __device__ __forceinline__ bool rec_hits(const float4 *__restrict__ r, const SubTile &st, int W) {
     constexpr int BB4 = Rec<KIND>::BB / 4;
     const float4 bb = r[BB4];
-    if (box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, W)) return true;
-    if (KIND != GS_PINHOLE) return false;
+    const bool box = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, W);
+    if (KIND != GS_PINHOLE) return box;
     const float4 c = r[2];
     const float cx = c.x + c.z, cy = c.y + c.w, r2 = r[3].x;
+    if (box) {
+        // small boxes (<= ELL_MIN px across, summed) are already tight: skip the ellipse test
+        const uint32_t bx = __float_as_uint(bb.z), by = __float_as_uint(bb.w);
+        const int span = (int)(bx >> 16) - (int)(bx & 0xffffu) + (int)(by >> 16) - (int)(by & 0xffffu);
+        if (span <= ELL_MIN || ellipse_hits(r, cx, cy, st)) return true;
+    }
     const float ddx = fmaxf(fmaxf((float)st.x0 + 0.5f - cx, cx - ((float)st.x1 + 0.5f)), 0.f);
     const float ddy = fmaxf(fmaxf((float)st.y0 + 0.5f - cy, cy - ((float)st.y1 + 0.5f)), 0.f);
     return fmaf(ddx, ddx, ddy * ddy) <= fmaf(r2, 1.0001f, 1e-3f);
@@ -467,21 +530,27 @@ __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const 
             cp_async_arrive(&pp.full[slot]);
         }
     } else {   // consumers
+        uint32_t dmask = __ballot_sync(FULL, done);
+        SubTile ast = (wdone || !ACTIVE_RECT<KIND>) ? st : active_rect(ry, done);
         for (uint32_t b = 0; b < nb; ++b) {
             const uint32_t gg = g + b, slot = gg % KSLOTS;
             mbar_wait(&pp.full[slot], (gg / KSLOTS) & 1u);
             const int cnt = *(volatile uint32_t *)&pp.stop_seq[slot] == gg ? -1 : (int)min(32u, e - (s + b * 32));
             if (cnt >= 0 && !wdone) {
                 const float4 *buf = ring + slot * 32 * S4;
-                const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, st, se.width);
+                const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, ast, se.width);
                 const uint32_t bits = __ballot_sync(FULL, hit);
                 if (bits && !done) {
                     eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
                     if (stopped && stop_b == NO_STOP) stop_b = b;
                 }
-                if (__all_sync(FULL, done)) {
+                const uint32_t dm = __ballot_sync(FULL, done);
+                if (dm == FULL) {
                     wdone = true;
                     if (lane == 0) atomicAdd(&pp.n_done, 1);
+                } else if (ACTIVE_RECT<KIND> && dm != dmask) {
+                    dmask = dm;
+                    ast = active_rect(ry, done);
                 }
             }
             if (cnt >= 0) ckpt_store(ck, b + 1, nb, a);
@@ -518,6 +587,8 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
     };
     const uint32_t nb = (e - s + 31) >> 5;
     stage(s, buf2);
+    uint32_t dmask = __ballot_sync(FULL, done);
+    SubTile ast = ACTIVE_RECT<KIND> ? active_rect(ry, done) : st;
     for (uint32_t b = 0; b < nb; ++b) {
         if (b + 1 < nb) {
             stage(s + (b + 1) * 32, buf2 + ((b + 1) & 1) * 32 * S4);
@@ -528,13 +599,15 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
         __syncwarp();
         const float4 *buf = buf2 + (b & 1) * 32 * S4;
         const int cnt = (int)min(32u, e - (s + b * 32));
-        const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, st, se.width);
+        const bool hit = lane < cnt && rec_hits<KIND>(buf + lane * S4, ast, se.width);
         const uint32_t bits = __ballot_sync(FULL, hit);
         if (bits && !done) {
             eval_bits<KIND, STATS>(bits, buf, ry, op, a, done, stopped, n_eval, n_comp);
             if (stopped && stop_b == NO_STOP) stop_b = b;
         }
-        if (__all_sync(FULL, done)) break;   // every later checkpoint is past every stop: never read
+        const uint32_t dm = __ballot_sync(FULL, done);
+        if (dm == FULL) break;   // every later checkpoint is past every stop: never read
+        if (ACTIVE_RECT<KIND> && dm != dmask) { dmask = dm; ast = active_rect(ry, done); }
         ckpt_store(ck, b + 1, nb, a);
         __syncwarp();
     }
@@ -722,7 +795,7 @@ __device__ __forceinline__ void render_body(
 // at 56 registers per thread (seven 5-warp CTAs per SM), fisheye and LiDAR at
 // 64 (fewer spills).
 template <bool STATS>
-__global__ void __maxnreg__(56) k_render_pinhole(
+__global__ void __maxnreg__(64) k_render_pinhole(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
