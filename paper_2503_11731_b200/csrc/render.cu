@@ -456,14 +456,28 @@ __device__ __forceinline__ void pipe_init(Pipe &pp, int nw) {
 
 // Evaluate the records of `buf` whose bit is set in the (warp-uniform) mask,
 // in order, for this lane's sample; stop at the first that ends the ray.
-// Records are taken in groups of four with compile-time offsets (empty groups
-// are skipped), which issues fewer instructions per record than a find-first-
-// set loop when the mask is dense and no more when it is sparse.
+// Pinhole masks are sparse after the ellipse test (≈3 records of 32 on the
+// Chunked forward camera): a find-first-set loop.  Fisheye and LiDAR masks
+// are denser: records in groups of four with compile-time offsets (empty
+// groups skipped), fewer instructions per record there (tools/sweep.py).
 template <int KIND, bool STATS>
 __device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restrict__ buf, const Ray &ry,
                                           const DevOpts &op, Acc &a, bool &done, bool &stopped,
                                           uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int S4 = Rec<KIND>::S4;
+    if (KIND == GS_PINHOLE) {   // sparse masks (after the ellipse test): one set bit at a time
+#pragma unroll 1
+        while (bits) {
+            const int u = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (!eval_record<KIND, STATS>(buf + u * S4, ry, op, a, n_eval, n_comp)) {
+                done = true;
+                stopped = true;
+                return;
+            }
+        }
+        return;
+    }
 #pragma unroll 1
     for (int jj = 0; jj < 32; jj += 4) {
         const uint32_t nib = (bits >> jj) & 0xfu;
