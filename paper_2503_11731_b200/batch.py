@@ -42,16 +42,29 @@ class FrameTimes:
 
 class BatchRenderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
-                 lidar_tile=(32, 1), grid_share: float | None = None):
+                 lidar_tile=(32, 1), grid_share: float | None = None, big_tile=(16, 16),
+                 big_tile_ratio: float = 16.0):
         """grid_share: fraction of the GPU's resident compositor CTA slots each
         frame's persistent grid takes (gs_opts.grid_share); default 2/n_streams
         (capped at 1), so about two frames composite at once and the other
-        streams' projection and binning kernels find free SMs."""
+        streams' projection and binning kernels find free SMs.
+        big_tile / big_tile_ratio: plan() bins a camera frame with the larger
+        `big_tile` when its surfels cover more than `big_tile_ratio` tiles each
+        on average at the default tile (large near surfels: the pair count,
+        hence the sort, shrinks ~2x while the compositor hardly slows; the
+        Chunked side cameras 1.89 -> 1.72 ms, the forward ones keep 16 x 8).
+        None disables it."""
         self.device = torch.device(device)
         n_streams = max(1, n_streams)
         o = gsr.gs_opts.from_buffer_copy(opts) if opts is not None else gsr.default_opts()
         o.grid_share = float(grid_share) if grid_share is not None else min(1.0, 2.0 / n_streams)
         self.lanes = [Renderer(surfels, o, device, lidar_tile) for _ in range(n_streams)]
+        self.big_opts = None
+        if big_tile is not None:
+            self.big_opts = gsr.gs_opts.from_buffer_copy(o)
+            self.big_opts.tile_w, self.big_opts.tile_h = int(big_tile[0]), int(big_tile[1])
+        self.big_tile_ratio = float(big_tile_ratio)
+        self.frame_opts = None
         self.streams = [torch.cuda.Stream(self.device) for _ in self.lanes]
         self.n = self.lanes[0].n
         self.caps = None
@@ -73,16 +86,26 @@ class BatchRenderer:
         box contains the ray (instrumented unsplit kernel)."""
         sensors = self.wrap(sensors)
         lane = self.lanes[0]
-        caps, contrib, evals = [], [], []
+        caps, contrib, evals, fopts = [], [], [], []
         for s in sensors:
-            _, d_np = lane.project(s)
-            caps.append(int(d_np.item()))
+            proj, d_np = lane.project(s)
+            P = int(d_np.item())
+            o = None
+            if self.big_opts is not None and s.kind != gsr.GS_LIDAR_SPINNING and P > 0:
+                V = int(proj[:4].view(torch.int32).item())   # header: visible surfels
+                if P > self.big_tile_ratio * V:
+                    o = self.big_opts
+                    _, d_np = lane.project(s, opts=o)
+                    P = int(d_np.item())
+            caps.append(P)
+            fopts.append(o)
         self.caps = caps
+        self.frame_opts = fopts
         self.ovf = torch.zeros(len(sensors), dtype=torch.int32, device=self.device)
         if stats:
-            for s, cap in zip(sensors, caps):
+            for s, cap, o in zip(sensors, caps, fopts):
                 st = torch.zeros((2, s.height, s.width), dtype=torch.int32, device=self.device)
-                lane.render(s, capacity=cap, stats=st)
+                lane.render(s, capacity=cap, stats=st, opts=o)
                 tot = st.view(2, -1).sum(dim=1, dtype=torch.int64).cpu()
                 contrib.append(int(tot[0]))
                 evals.append(int(tot[1]))
@@ -109,7 +132,7 @@ class BatchRenderer:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if want else None
             with torch.cuda.stream(self.streams[k]):
                 self.lanes[k].render(s, out=outs[i], capacity=self.caps[i], events=ev,
-                                     overflow=self.ovf[i:i + 1])
+                                     overflow=self.ovf[i:i + 1], opts=self.frame_opts[i])
                 if on_frame is not None:
                     on_frame(i, self.streams[k])
             evs.append(ev)
@@ -124,6 +147,10 @@ class BatchRenderer:
                 times.sort.append(ev[1].elapsed_time(ev[2]))
                 times.render.append(ev[2].elapsed_time(ev[3]))
         return outs
+
+    def opts_of(self, i: int):
+        """Options frame i of the planned batch is rendered with (None: the lane's default)."""
+        return self.frame_opts[i]
 
     def overflowed(self):
         """Indices of frames of the last render() whose pair capacity was exceeded."""

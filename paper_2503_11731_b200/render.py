@@ -65,8 +65,8 @@ class Renderer:
     def opts_for(self, sensor) -> gsr.gs_opts:
         return self.lidar_opts if sensor.kind == gsr.GS_LIDAR_SPINNING else self.cam_opts
 
-    def project(self, sensor: gsr.Sensor, stream=None):
-        self.opts = self.opts_for(sensor)
+    def project(self, sensor: gsr.Sensor, stream=None, opts: gsr.gs_opts | None = None):
+        self.opts = opts if opts is not None else self.opts_for(sensor)
         st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         proj = self._get("proj", gsr.gs_projected_bytes(self.n, sensor.kind))
         d_np = self._get("np", 8)[:8].view(torch.int64)
@@ -75,14 +75,16 @@ class Renderer:
 
     def render(self, sensor, out: torch.Tensor | None = None, capacity: int | None = None,
                keys: bool = False, stream=None, stats: torch.Tensor | None = None,
-               events=None, overflow: torch.Tensor | None = None) -> torch.Tensor:
+               events=None, overflow: torch.Tensor | None = None,
+               opts: gsr.gs_opts | None = None) -> torch.Tensor:
         """Render one frame; returns a planar fp32 tensor [C,H,W] (C = 8 for
         cameras: r,g,b,depth,nx,ny,nz,alpha; 4 for LiDAR: range, intensity,
         raydrop, alpha).  stats: optional int32 [2,H,W] (composited, evaluated
         pairs per sample).  events: optional 4 CUDA events recorded before
         gs_project, gs_bin_sort, the render call and after it.  overflow:
         optional int32 device slot for gs_bin_sort's overflow flag (default:
-        a buffer owned by the renderer)."""
+        a buffer owned by the renderer).  opts: this frame's options instead
+        of the renderer's (e.g. another tile shape)."""
         if not isinstance(sensor, gsr.Sensor):
             sensor = gsr.Sensor(sensor)
         self.opts = self.opts_for(sensor)
@@ -90,7 +92,7 @@ class Renderer:
         st = stream if stream is not None else torch_stream.cuda_stream
         if events is not None:
             events[0].record(torch_stream)
-        proj, d_np = self.project(sensor, st)
+        proj, d_np = self.project(sensor, st, opts)
         if events is not None:
             events[1].record(torch_stream)
         if capacity is None:

@@ -216,9 +216,11 @@ def test_capacity_overflow_and_graph_mode(gsr_mod):
 
 
 # ---------------------------------------------------------------- batch / pipeline paths
-def test_batch_renderer_matches_single_frames(gsr_mod):
-    """BatchRenderer (capacity mode, two streams, per-frame overflow slots)
-    gives the same bytes as rendering each frame alone."""
+@pytest.mark.parametrize("ratio", [16.0, 0.0])
+def test_batch_renderer_matches_single_frames(gsr_mod, ratio):
+    """BatchRenderer (capacity mode, two streams, per-frame overflow slots,
+    per-frame tile choice; ratio 0 sends every camera to the big tile) gives
+    the same bytes as rendering each frame alone with the planned options."""
     from paper_2503_11731_b200.batch import BatchRenderer
     from paper_2503_11731_b200.render import Renderer, to_device
     rng = np.random.default_rng(41)
@@ -227,15 +229,17 @@ def test_batch_renderer_matches_single_frames(gsr_mod):
                for y in (0, 90, 180)]
     sensors.append(sg.lidar64(sg.lidar_pose([0, 1.8, 10.0]), height=16, width=256))
     dev = to_device(s)
-    br = BatchRenderer(dev, n_streams=2)
+    br = BatchRenderer(dev, n_streams=2, big_tile_ratio=ratio)
     br.plan(sensors)
+    if ratio == 0.0:
+        assert all((br.opts_of(i) is not None) == (i < 3) for i in range(4))
     outs = br.alloc_outputs(br.wrap(sensors))
     br.render(sensors, outs)
     torch.cuda.synchronize()
     assert br.overflowed() == []
     single = Renderer(dev)
-    for se, o in zip(sensors, outs):
-        ref = single.render(se).cpu().numpy()
+    for i, (se, o) in enumerate(zip(sensors, outs)):
+        ref = single.render(se, opts=br.opts_of(i)).cpu().numpy()   # same tile shape as planned
         np.testing.assert_array_equal(o.cpu().numpy(), ref)
 
 
