@@ -407,15 +407,15 @@ def run_gsr(args):
     # context: the same launches one at a time on one stream (no overlap), a sample of frames
     iso_idx = [i for i in idx if (i // 7) % 8 == 0] or idx
     lane = br.lanes[0]
-    share0 = (lane.cam_opts.grid_share, lane.lidar_opts.grid_share)
-    lane.cam_opts.grid_share = lane.lidar_opts.grid_share = 1.0   # alone on the GPU: the full grid
     iso_ev = []
     for i in iso_idx:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        lane.render(sensors[i], out=outs[i], capacity=br.caps[i], events=ev, overflow=br.ovf[i:i + 1])
+        o = gsr.gs_opts.from_buffer_copy(br.opts_of(i) or lane.opts_for(sensors[i]))
+        o.grid_share = 1.0   # alone on the GPU: the full grid
+        lane.render(sensors[i], out=outs[i], capacity=br.caps[i], events=ev, overflow=br.ovf[i:i + 1], opts=o)
         iso_ev.append(ev)
     torch.cuda.synchronize(device)
-    lane.cam_opts.grid_share, lane.lidar_opts.grid_share = share0
+    assert not br.overflowed(), "pair capacity exceeded in the isolated re-renders"
     t_iso = float(np.mean([ev[2].elapsed_time(ev[3]) for ev in iso_ev])) * 1e-3
     instr_iso = float(np.mean([contrib[i] for i in iso_idx])) * INSTR_PER_PAIR[dom_kind]
     roofline = {"kernel": f"gs_render_camera ({'pinhole' if dom_kind == 0 else 'kind %d' % dom_kind})",
