@@ -465,7 +465,7 @@ __device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restric
                                           const DevOpts &op, Acc &a, bool &done, bool &stopped,
                                           uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int S4 = Rec<KIND>::S4;
-    if (KIND == GS_PINHOLE) {   // sparse masks (after the ellipse test): one set bit at a time
+    if constexpr (KIND == GS_PINHOLE) {   // sparse masks (after the ellipse test): one set bit at a time
 #pragma unroll 1
         while (bits) {
             const int u = __ffs(bits) - 1;
@@ -476,20 +476,20 @@ __device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restric
                 return;
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll 1
-    for (int jj = 0; jj < 32; jj += 4) {
-        const uint32_t nib = (bits >> jj) & 0xfu;
-        if (!nib) continue;
-        const float4 *b4 = buf + jj * S4;
+        for (int jj = 0; jj < 32; jj += 4) {
+            const uint32_t nib = (bits >> jj) & 0xfu;
+            if (!nib) continue;
+            const float4 *b4 = buf + jj * S4;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (nib & (1u << u)) {
-                if (!eval_record<KIND, STATS>(b4 + u * S4, ry, op, a, n_eval, n_comp)) {
-                    done = true;
-                    stopped = true;
-                    return;
+            for (int u = 0; u < 4; ++u) {
+                if (nib & (1u << u)) {
+                    if (!eval_record<KIND, STATS>(b4 + u * S4, ry, op, a, n_eval, n_comp)) {
+                        done = true;
+                        stopped = true;
+                        return;
+                    }
                 }
             }
         }
