@@ -27,12 +27,15 @@ __device__ __forceinline__ double pinned_row(const float *Rr, float tk, float mx
     return __dadd_rn(__dadd_rn(__dadd_rn(a, b), c), (double)tk);
 }
 
+// Pixel-space box in fp32: its points are rounded once from fp64 (or formed in
+// fp32 from fp64 operands) -- errors of a few 1e-7 relative, far inside the
+// 1e-3 px + 1e-6 |x| margin of box_to_tiles.
 struct Box {
-    double x0, x1, y0, y1;
-    __device__ void init() { x0 = y0 = 1e300; x1 = y1 = -1e300; }
-    __device__ void add(double x, double y) {
-        x0 = fmin(x0, x); x1 = fmax(x1, x);
-        y0 = fmin(y0, y); y1 = fmax(y1, y);
+    float x0, x1, y0, y1;
+    __device__ void init() { x0 = y0 = __int_as_float(0x7f800000); x1 = y1 = -__int_as_float(0x7f800000); }
+    __device__ void add(float x, float y) {
+        x0 = fminf(x0, x); x1 = fmaxf(x1, x);
+        y0 = fminf(y0, y); y1 = fmaxf(y1, y);
     }
 };
 
@@ -68,8 +71,9 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
         const double Y = mu[1] + c * a[1] + s * b[1];
         const double Z = mu[2] + c * a[2] + s * b[2];
         if (Z >= nearp * (1.0 - 1e-9)) {
-            const double iz = 1.0 / fmax(Z, nearp * (1.0 - 1e-9));
-            box.add((double)se.fx * X * iz + (double)se.cx, (double)se.fy * Y * iz + (double)se.cy);
+            // the sum above in fp64 (cancellation); the projection of the point in fp32
+            const float iz = __frcp_rn((float)fmax(Z, nearp * (1.0 - 1e-9)));
+            box.add(fmaf(se.fx * (float)X, iz, se.cx), fmaf(se.fy * (float)Y, iz, se.cy));
         }
     };
     auto solve = [&](double A, double B, double C, bool strict) {
@@ -95,16 +99,17 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
 // pixel range [i0,i1] -> tile range; returns false if empty
 __device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw, int th,
                                              int &tx0, int &ty0, int &tx1, int &ty1, int pb[4]) {
-    const double m = 1e-3;
-    double x0 = bx.x0 - m - 1e-6 * fabs(bx.x0), x1 = bx.x1 + m + 1e-6 * fabs(bx.x1);
-    double y0 = bx.y0 - m - 1e-6 * fabs(bx.y0), y1 = bx.y1 + m + 1e-6 * fabs(bx.y1);
+    const float m = 1e-3f;
+    float x0 = bx.x0 - m - 1e-6f * fabsf(bx.x0), x1 = bx.x1 + m + 1e-6f * fabsf(bx.x1);
+    float y0 = bx.y0 - m - 1e-6f * fabsf(bx.y0), y1 = bx.y1 + m + 1e-6f * fabsf(bx.y1);
     if (!(x0 <= x1) || !(y0 <= y1)) {   // NaN: whole image (conservative)
-        x0 = y0 = -1e30; x1 = y1 = 1e30;
+        x0 = y0 = -1e30f; x1 = y1 = 1e30f;
     }
-    const double i0 = ceil(x0 - 0.5), i1 = floor(x1 - 0.5);
-    const double j0 = ceil(y0 - 0.5), j1 = floor(y1 - 0.5);
-    const int ci0 = (int)fmax(i0, 0.0), ci1 = (int)fmin(i1, (double)(W - 1));
-    const int cj0 = (int)fmax(j0, 0.0), cj1 = (int)fmin(j1, (double)(H - 1));
+    // clamp before the int conversion (|x| may be huge or infinite)
+    const float i0 = ceilf(fmaxf(x0 - 0.5f, -1.f)), i1 = floorf(fminf(x1 - 0.5f, (float)W));
+    const float j0 = ceilf(fmaxf(y0 - 0.5f, -1.f)), j1 = floorf(fminf(y1 - 0.5f, (float)H));
+    const int ci0 = max((int)i0, 0), ci1 = min((int)i1, W - 1);
+    const int cj0 = max((int)j0, 0), cj1 = min((int)j1, H - 1);
     if (ci0 > ci1 || cj0 > cj1) return false;
     tx0 = ci0 / tw; tx1 = ci1 / tw; ty0 = cj0 / th; ty1 = cj1 / th;
     pb[0] = ci0; pb[1] = cj0; pb[2] = ci1; pb[3] = cj1;
