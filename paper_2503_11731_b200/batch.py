@@ -148,6 +148,12 @@ class BatchRenderer:
                 times.render.append(ev[2].elapsed_time(ev[3]))
         return outs
 
+    def set_surfels(self, surfels: dict):
+        """Render from another device copy of the same surfel set (same count and
+        layout; e.g. a double buffer that the next batch is uploaded into)."""
+        for lane in self.lanes:
+            lane.set_surfels(surfels)
+
     def opts_of(self, i: int):
         """Options frame i of the planned batch is rendered with (None: the lane's default)."""
         return self.frame_opts[i]

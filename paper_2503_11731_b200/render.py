@@ -51,6 +51,12 @@ class Renderer:
         self._buf = {}
         self.last_pairs = None
 
+    def set_surfels(self, surfels: dict):
+        """Point the renderer at another device copy of a surfel set of the same size."""
+        assert int(surfels["means"].shape[0]) == self.n
+        self.t = surfels
+        self.struct = gsr.surfels_struct(surfels)
+
     # buffers are cached per (name) and grown on demand
     def _get(self, name, nbytes):
         b = self._buf.get(name)
