@@ -858,8 +858,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_compact(const uint32_t *__rest
     if (warp == 0) {
         const unsigned long long tv = warp_excl_scan_smem(s_wv, SCAN_THREADS / 32);
         const unsigned long long tp = warp_excl_scan_smem(s_wp, SCAN_THREADS / 32);
-        const unsigned long long ev = lookback_warp_u64(st_vis, tile, tv);
-        const unsigned long long ep = lookback_warp_u64(st_pairs, tile, tp);
+        unsigned long long ev, ep;
+        if (nsurf < (1ll << 25)) {   // one look-back for both: pairs << 25 | visible (62 value bits)
+            const unsigned long long eq = lookback_warp_u64(st_vis, tile, (tp << 25) | tv);
+            ev = eq & ((1ull << 25) - 1);
+            ep = eq >> 25;
+        } else {
+            ev = lookback_warp_u64(st_vis, tile, tv);
+            ep = lookback_warp_u64(st_pairs, tile, tp);
+        }
         if (lane == 0) {
             s_excl_v = ev;
             const int64_t end = (int64_t)(tile + 1) * SCAN_TILE;
