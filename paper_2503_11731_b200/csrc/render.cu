@@ -374,13 +374,20 @@ struct Ckpt {
     float *base;     // this segment's NCP checkpoint blocks, or nullptr
     uint32_t cb;     // batches between checkpoints
     int npix, t;     // samples per tile, this thread's sample
+    uint32_t next;   // batches walked when checkpoint c is due (~0u: none)
+    uint32_t c;      // next checkpoint, 1..NCP
 };
 
-__device__ __forceinline__ void ckpt_store(const Ckpt &ck, uint32_t b_done, uint32_t nb, const Acc &a) {
+__device__ __forceinline__ Ckpt make_ckpt(float *base, uint32_t cb, int npix, int t) {
+    return Ckpt{base, cb, npix, t, base ? cb : ~0u, 1u};
+}
+
+__device__ __forceinline__ void ckpt_store(Ckpt &ck, uint32_t b_done, uint32_t nb, const Acc &a) {
     // b_done batches have been walked; checkpoint c sits at c * cb batches
-    if (!ck.base || b_done % ck.cb != 0u || b_done >= nb) return;
-    const uint32_t c = b_done / ck.cb;
-    if (c < 1u || c > (uint32_t)NCP) return;
+    if (b_done != ck.next) return;
+    const uint32_t c = ck.c++;
+    ck.next = ck.c <= (uint32_t)NCP ? ck.next + ck.cb : ~0u;
+    if (b_done >= nb) return;
     float *p = ck.base + (size_t)(c - 1) * NPART * ck.npix + ck.t;
     const int n = ck.npix;
     p[0 * n] = a.T; p[1 * n] = a.A; p[2 * n] = a.c0; p[3 * n] = a.c1; p[4 * n] = a.c2;
@@ -505,7 +512,7 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *ring, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
-                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, const Ckpt &ck,
+                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, Ckpt &ck,
                                      uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
@@ -583,7 +590,7 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                           uint32_t s, uint32_t e, float4 *buf2, const SubTile &st, const Ray &ry,
                                           const DevSensor &se, const DevOpts &op, Acc &a, bool &done,
-                                          bool &stopped, uint32_t &stop_b, const Ckpt &ck, uint32_t &n_eval,
+                                          bool &stopped, uint32_t &stop_b, Ckpt &ck, uint32_t &n_eval,
                                           uint32_t &n_comp) {
     constexpr int R4 = Rec<KIND>::F / 4, S4 = Rec<KIND>::S4;
     constexpr int BB4 = Rec<KIND>::BB / 4;
@@ -633,7 +640,7 @@ template <int KIND, bool STATS>
 __device__ __forceinline__ void walk(bool piped, const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *smem, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
-                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, const Ckpt &ck,
+                                     Acc &a, bool &done, bool &stopped, uint32_t &stop_b, Ckpt &ck,
                                      uint32_t &n_eval, uint32_t &n_comp) {
     if (piped)
         walk_pipe<KIND, STATS>(rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
@@ -784,8 +791,8 @@ __device__ __forceinline__ void render_body(
         Acc a = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !ry.valid, stopped = false;
         uint32_t n_eval = 0, n_comp = 0, stop_b = NO_STOP;
-        Ckpt ck = {nullptr, cb, npix, t};
-        if (ns > 1 && cons) ck.base = ckpt + (size_t)(split_base[tile] + seg) * NCP * NPART * npix;
+        Ckpt ck = make_ckpt(ns > 1 && cons ? ckpt + (size_t)(split_base[tile] + seg) * NCP * NPART * npix : nullptr,
+                            cb, npix, t);
         walk<KIND, STATS>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
                           n_eval, n_comp);
         if (!cons) continue;
@@ -957,7 +964,7 @@ __global__ void __maxnreg__(80) k_rewalk(
         Acc r = {m[0], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool done = !mine, stopped = false;
         uint32_t ne = 0, nc = 0, sb = NO_STOP;
-        const Ckpt ck = {nullptr, 1u, npix, t};
+        Ckpt ck = make_ckpt(nullptr, 1u, npix, t);
         // the chunk between checkpoints c and c+1 of segment k (the ray stops inside it)
         const uint32_t seg_s = rg.x + k * L, seg_e = min(rg.y, seg_s + L);
         const uint32_t s = min(seg_e, seg_s + c * cb * 32u), e = min(seg_e, seg_s + (c + 1u) * cb * 32u);
