@@ -210,10 +210,12 @@ __device__ __forceinline__ bool in_box(uint32_t bx, uint32_t by, int x, int xw, 
 
 // Does a record's conservative pixel box (packed u16 pairs; LiDAR columns may
 // run past width-1 = azimuth wrap) touch the sub-tile?
+template <bool WRAP>
 __device__ __forceinline__ bool box_hits(uint32_t bx, uint32_t by, const SubTile &st, int W) {
     const int x0 = (int)(bx & 0xffffu), x1 = (int)(bx >> 16);
     const int y0 = (int)(by & 0xffffu), y1 = (int)(by >> 16);
-    const bool okx = (x0 <= st.x1 && x1 >= st.x0) || (x0 <= st.x1 + W && x1 >= st.x0 + W);
+    bool okx = x0 <= st.x1 && x1 >= st.x0;
+    if (WRAP) okx = okx || (x0 <= st.x1 + W && x1 >= st.x0 + W);   // LiDAR azimuth seam
     return okx && y0 <= st.y1 && y1 >= st.y0;
 }
 
@@ -265,7 +267,7 @@ template <int KIND>
 __device__ __forceinline__ bool rec_hits(const float4 *__restrict__ r, const SubTile &st, int W) {
     constexpr int BB4 = Rec<KIND>::BB / 4;
     const float4 bb = r[BB4];
-    const bool box = box_hits(__float_as_uint(bb.z), __float_as_uint(bb.w), st, W);
+    const bool box = box_hits<KIND == GS_LIDAR_SPINNING>(__float_as_uint(bb.z), __float_as_uint(bb.w), st, W);
     if (KIND != GS_PINHOLE) return box;
     const float4 c = r[2];
     const float cx = c.x + c.z, cy = c.y + c.w, r2 = r[3].x;
