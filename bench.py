@@ -178,8 +178,8 @@ def run_reference(args):
         tot_rays += n
         tot_t += t
     value = tot_rays / tot_t / 1e6
-    desc.update(parallelism="oracle (CPU)", n_gpus_requested=args.gpus)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+    desc.update(parallelism="oracle (CPU)", gpus_used=0)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (scenegen, BASELINE.json configs)", "config": desc,
