@@ -245,7 +245,7 @@ __device__ __forceinline__ bool ellipse_hits(const float4 *__restrict__ r, float
     const float B0 = -R * qc * g1.x, B1 = -R * qc * g1.y, C = -R * qc * qc;
     const float X0 = (float)st.x0 + 0.49f - cx, X1 = (float)st.x1 + 0.51f - cx;
     const float Y0 = (float)st.y0 + 0.49f - cy, Y1 = (float)st.y1 + 0.51f - cy;
-    const float idet = 1.f / det;
+    const float idet = __fdividef(1.f, det);   // approximate: it only places the test points
     const float sx = (M01 * B1 - M11 * B0) * idet, sy = (M01 * B0 - M00 * B1) * idet;
     if (sx >= X0 && sx <= X1 && sy >= Y0 && sy <= Y1) return true;
     // slack 2e-3 R w_max^2, w_max bounding |a2.d + qc| over the rectangle (Q's terms there)
@@ -254,7 +254,7 @@ __device__ __forceinline__ bool ellipse_hits(const float4 *__restrict__ r, float
     auto q = [&](float x, float y) {
         return fmaf(x, fmaf(M00, x, 2.f * fmaf(M01, y, B0)), fmaf(y, fmaf(M11, y, 2.f * B1), C));
     };
-    const float i00 = 1.f / M00, i11 = 1.f / M11;
+    const float i00 = __fdividef(1.f, M00), i11 = __fdividef(1.f, M11);
     const float xa = fminf(fmaxf(-(M01 * Y0 + B0) * i00, X0), X1);
     const float xb = fminf(fmaxf(-(M01 * Y1 + B0) * i00, X0), X1);
     const float ya = fminf(fmaxf(-(M01 * X0 + B1) * i11, Y0), Y1);
