@@ -5,8 +5,9 @@
  *   gs_project  ->  gs_bin_sort  ->  gs_render_camera | gs_render_lidar
  *
  * Conventions for every entry point
- *   - Ownership: the caller owns every buffer.  The library never allocates,
- *     keeps no global state and holds no pointer after a call returns.
+ *   - Ownership: the caller owns every buffer.  The library never allocates
+ *     and holds no pointer after a call returns; its only process state is a
+ *     relaxed kernel-launch counter and a cache of per-kernel occupancies.
  *   - Memory: pointers named d_* and all array pointers inside gs_surfels and
  *     the output/work buffers are DEVICE pointers (cudaMalloc / torch);
  *     gs_sensor.beam_elevation is a HOST pointer (copied into kernel
@@ -26,7 +27,11 @@
  *   - Reentrancy: calls are pure functions of their inputs; concurrent calls
  *     on different streams with distinct output buffers are safe.
  *   - Determinism: no floating-point atomics; outputs are bitwise
- *     reproducible for identical inputs, independent of tile shape.
+ *     reproducible for identical inputs and options on the same GPU type.
+ *     Unsplit tile lists (split_len = INT32_MAX) composite the same per-sample
+ *     sequence for every tile shape (bitwise equal images); split lists (whose
+ *     adaptive length depends on the SM count and grid_share) differ only by
+ *     fp32 rounding of the merge.
  *
  * Sizing protocol (the pair count P is only known on the device):
  *   simple mode: gs_project, synchronise, read *d_num_pairs, allocate P
