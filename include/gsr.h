@@ -229,8 +229,9 @@ int32_t gs_record_bytes(int32_t kind);
 /* Byte offsets inside the projected buffer (debug/tests): offs[0] records
  * [n, gs_record_bytes], offs[1] tile rects [n] int16x4 (x0,y0,x1,y1; x1 may
  * exceed the tile columns for LiDAR azimuth wrap), offs[2] depth keys [n] u32
- * (fp32 bits; 0xffffffff if culled), offs[3] pair counts [n] u32, offs[4]
- * total bytes.  The header at offset 0 holds u32 n_visible at +0 and int64
+ * (fp32 bits), offs[3] pair counts [n] u32 (0 for every culled surfel),
+ * offs[4] total bytes.  Rects and keys are defined where the count is > 0
+ * (surfels dropped by the conservative pre-cull keep whatever was there).  The header at offset 0 holds u32 n_visible at +0 and int64
  * num_pairs at +8. */
 void gs_projected_offsets(int64_t n, int32_t kind, size_t offs[5]);
 

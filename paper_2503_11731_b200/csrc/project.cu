@@ -461,11 +461,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
             uint32_t kb;
             const bool c = cull_one<KIND>(s, se, op, i, kb, sb);
             if (c) { flags |= 1u << j; ++cnt; }
-            // every surfel gets the culled outputs here (full, coalesced lines);
-            // k_project overwrites those of the candidates it finds visible
-            keys[i] = 0xffffffffu;
+            // every surfel gets a zero pair count here (coalesced); k_project writes
+            // count, key and rect of every candidate.  Nothing reads the key or rect
+            // of a culled surfel, so those are not written for it.
             counts[i] = 0;
-            rect[i] = make_short4(0, 0, -1, -1);
         }
     }
     // per round j: CTA-wide exclusive rank of this thread's item among the passing items of round j

@@ -146,6 +146,11 @@ class Renderer:
         rect = proj[offs["rect"]: offs["rect"] + 8 * n].view(torch.int16).view(n, 4).cpu().numpy()
         key = proj[offs["key"]: offs["key"] + 4 * n].view(torch.int32).cpu().numpy().view(np.uint32)
         cnt = proj[offs["count"]: offs["count"] + 4 * n].view(torch.int32).cpu().numpy()
+        culled = cnt == 0   # rect and key are only defined where the count is > 0 (gsr.h)
+        rect = rect.copy()
+        rect[culled] = (0, 0, -1, -1)
+        key = key.copy()
+        key[culled] = 0xFFFFFFFF
         P = int(proj[8:16].view(torch.int64).item())
         vals = L["values"][:P].cpu().numpy().view(np.uint32)
         keys = L["keys"][:P].cpu().numpy().view(np.uint64) if L["keys"] is not None else None
