@@ -138,6 +138,8 @@ static DevSensor make_dev_sensor(const gs_sensor *s, const gs_opts *o) {
     d.height = s->height;
     d.tw = o->tile_w;
     d.th = o->tile_h;
+    d.mtw = (uint32_t)(((1ull << 32) + (uint64_t)d.tw - 1) / (uint64_t)d.tw);
+    d.mth = (uint32_t)(((1ull << 32) + (uint64_t)d.th - 1) / (uint64_t)d.th);
     d.ntx = (s->width + o->tile_w - 1) / o->tile_w;
     d.nty = (s->height + o->tile_h - 1) / o->tile_h;
     warp_subtile(s->kind, o->tile_w, o->tile_h, &d.sw, &d.sh);

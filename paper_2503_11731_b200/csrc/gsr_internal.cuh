@@ -23,6 +23,7 @@ struct DevSensor {
     float az0, az_step;
     int32_t nbeams;
     int32_t full_turn;          // LiDAR: width*az_step covers 2pi (azimuth wraps)
+    uint32_t mtw, mth;          // ceil(2^32 / tw), ceil(2^32 / th) (0 for 1): exact division of pixel indices (n d < 2^32)
     float beam[GS_MAX_BEAMS];
     float sbeam[GS_MAX_BEAMS];  // sin(beam), fp64-evaluated, rounded to fp32
 };

@@ -72,7 +72,7 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
         const double Z = mu[2] + c * a[2] + s * b[2];
         if (Z >= nearp * (1.0 - 1e-9)) {
             // the sum above in fp64 (cancellation); the projection of the point in fp32
-            const float iz = __frcp_rn((float)fmax(Z, nearp * (1.0 - 1e-9)));
+            const float iz = __fdividef(1.f, (float)fmax(Z, nearp * (1.0 - 1e-9)));   // 2 ulp: margins cover it
             box.add(fmaf(se.fx * (float)X, iz, se.cx), fmaf(se.fy * (float)Y, iz, se.cy));
         }
     };
@@ -96,8 +96,11 @@ __device__ void pinhole_disk_bound(const DevSensor &se, double nearp, const doub
     solve(a[2], b[2], mu[2] - nearp, true);   // chord on the near plane
 }
 
+// n / d from m = ceil(2^32 / d) (m == 0 encodes d == 1, whose m does not fit)
+__device__ __forceinline__ uint32_t tdiv(uint32_t n, uint32_t m) { return m ? __umulhi(n, m) : n; }
+
 // pixel range [i0,i1] -> tile range; returns false if empty
-__device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw, int th,
+__device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, uint32_t mtw, uint32_t mth,
                                              int &tx0, int &ty0, int &tx1, int &ty1, int pb[4]) {
     const float m = 1e-3f;
     float x0 = bx.x0 - m - 1e-6f * fabsf(bx.x0), x1 = bx.x1 + m + 1e-6f * fabsf(bx.x1);
@@ -111,7 +114,10 @@ __device__ __forceinline__ bool box_to_tiles(const Box &bx, int W, int H, int tw
     const int ci0 = max((int)i0, 0), ci1 = min((int)i1, W - 1);
     const int cj0 = max((int)j0, 0), cj1 = min((int)j1, H - 1);
     if (ci0 > ci1 || cj0 > cj1) return false;
-    tx0 = ci0 / tw; tx1 = ci1 / tw; ty0 = cj0 / th; ty1 = cj1 / th;
+    // n / d as umulhi(n, ceil(2^32 / d)): exact while n d < 2^32 (here n < 2^18, d <= 512):
+    // the error n (m d - 2^32) / (d 2^32) < n / 2^32 < 1/d cannot cross an integer, as n mod d <= d - 1
+    tx0 = (int)tdiv((uint32_t)ci0, mtw); tx1 = (int)tdiv((uint32_t)ci1, mtw);
+    ty0 = (int)tdiv((uint32_t)cj0, mth); ty1 = (int)tdiv((uint32_t)cj1, mth);
     pb[0] = ci0; pb[1] = cj0; pb[2] = ci1; pb[3] = cj1;
     return true;
 }
@@ -566,7 +572,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             {   // pixel box of the 3-sigma disk alone (the record's box; the low-pass disc is
                 // tested from the centre and radius by the compositor); empty: x0 = y0 = 0xffff
                 int ttx0, tty0, ttx1, tty1, cb[4];
-                if (box_to_tiles(bx, se.width, se.height, se.tw, se.th, ttx0, tty0, ttx1, tty1, cb)) {
+                if (box_to_tiles(bx, se.width, se.height, se.mtw, se.mth, ttx0, tty0, ttx1, tty1, cb)) {
                     for (int k = 0; k < 4; ++k) cpb[k] = cb[k];
                 }
             }
@@ -575,7 +581,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             const double cy = (double)se.fy * mu[1] * iz + (double)se.cy;
             bx.add(cx - rlp, cy - rlp);
             bx.add(cx + rlp, cy + rlp);
-            vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1, pb);
+            vis = box_to_tiles(bx, se.width, se.height, se.mtw, se.mth, tx0, ty0, tx1, ty1, pb);
         } else {
             const double r = sqrt(dot3(mu, mu)), ir = 1.0 / r;
             const double m[3] = {mu[0] * ir, mu[1] * ir, mu[2] * ir};
@@ -630,7 +636,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                 fisheye_project(se, mu, cxp, cyp);
                 bx.add(cxp - rlp, cyp - rlp);
                 bx.add(cxp + rlp, cyp + rlp);
-                vis = box_to_tiles(bx, se.width, se.height, se.tw, se.th, tx0, ty0, tx1, ty1, pb);
+                vis = box_to_tiles(bx, se.width, se.height, se.mtw, se.mth, tx0, ty0, tx1, ty1, pb);
             } else {   // LiDAR: angular box with azimuth wrap
                 const int W = se.width;
                 int r0 = 0, r1 = se.nbeams - 1, c0 = 0, c1 = W - 1;
@@ -677,12 +683,12 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                         tx0 = 0; tx1 = ntx - 1;
                         c0 = 0; c1 = W - 1;
                     } else {
-                        tx0 = c0 / se.tw;
-                        tx1 = c1 < W ? c1 / se.tw : ntx + (c1 - W) / se.tw;
+                        tx0 = (int)tdiv((uint32_t)c0, se.mtw);   // exact division, as in box_to_tiles
+                        tx1 = c1 < W ? (int)tdiv((uint32_t)c1, se.mtw) : ntx + (int)tdiv((uint32_t)(c1 - W), se.mtw);
                         if (tx1 - tx0 + 1 >= ntx) { tx0 = 0; tx1 = ntx - 1; c0 = 0; c1 = W - 1; }
                     }
-                    ty0 = r0 / se.th;
-                    ty1 = r1 / se.th;
+                    ty0 = (int)tdiv((uint32_t)r0, se.mth);
+                    ty1 = (int)tdiv((uint32_t)r1, se.mth);
                     pb[0] = c0; pb[1] = r0; pb[2] = c1; pb[3] = r1;   // c1 may exceed W-1 (wrap)
                 }
             }

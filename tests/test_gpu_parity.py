@@ -123,7 +123,7 @@ def test_binning_bit_exact_lidar_wrap(gsr_mod):
     np.testing.assert_array_equal(b["ranges"], ranges)
 
 
-@pytest.mark.parametrize("tiles", [(8, 4), (32, 8), (16, 32), (24, 12), (32, 2)])
+@pytest.mark.parametrize("tiles", [(8, 4), (32, 8), (16, 32), (24, 12), (32, 2), (32, 1), (128, 1)])
 def test_tile_shape_invariance_bitwise(gsr_mod, tiles):
     """Unsplit tile lists: per-pair arithmetic never depends on the tile."""
     c = sg.mid(seed=11, n=20_000, width=200, height=150, f=125.0)
