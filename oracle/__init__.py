@@ -68,6 +68,10 @@ def lib():
         P = C.POINTER
         _lib.or_render.argtypes = [P(_Scene), P(_Sensor), P(_Opts), C.c_int64, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        _lib.or_render_variants.argtypes = [P(_Scene), P(_Sensor), P(_Opts), C.c_int64, C.c_void_p,
+                                            C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        _lib.or_cond_uv.argtypes = [C.c_void_p, C.c_void_p]
+        _lib.or_cond_uv.restype = C.c_double
         _lib.or_keys.argtypes = [P(_Scene), P(_Sensor), P(_Opts), C.c_void_p, C.c_void_p]
         _lib.or_surfel.argtypes = [P(_Scene), P(_Sensor), P(_Opts), C.c_int64, C.c_void_p]
         _lib.or_ray.argtypes = [P(_Sensor), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
@@ -152,6 +156,32 @@ def render(surfels, sensor, rays=None, nthreads=0, **opts):
     if rc != 0:
         raise RuntimeError(f"or_render failed: {rc}")
     return out, flags, ncon
+
+
+def variants(surfels, sensor, rays, max_var=256, nthreads=0, **opts):
+    """Near-decision variants of each ray: returns
+    (var [n, max_var, 8] f64, nvar [n] i32, seen [n] u8).  var[r, :nvar[r]]
+    are the admissible composites (variant 0 = the nominal one); nvar[r] >
+    max_var marks an unresolved ray."""
+    keep = _Keep()
+    sc, se, op = _scene(surfels, keep), _sensor(sensor, keep), _opts(**opts)
+    rays = np.ascontiguousarray(rays, dtype=np.int64)
+    n = rays.size
+    var = np.zeros((n, max_var, 8), np.float64)
+    nvar = np.zeros(n, np.int32)
+    seen = np.zeros(n, np.uint8)
+    rc = lib().or_render_variants(C.byref(sc), C.byref(se), C.byref(op), n, rays.ctypes.data,
+                                  int(max_var), var.ctypes.data, nvar.ctypes.data, seen.ctypes.data,
+                                  int(nthreads))
+    if rc != 0:
+        raise RuntimeError(f"or_render_variants failed: {rc}")
+    return var, nvar, seen
+
+
+def cond_uv(M, d):
+    M = np.ascontiguousarray(M, np.float64)
+    d = np.ascontiguousarray(d, np.float64)
+    return lib().or_cond_uv(M.ctypes.data, d.ctypes.data)
 
 
 def keys(surfels, sensor, **opts):

@@ -31,6 +31,9 @@
 #endif
 
 #define OR_PI 3.14159265358979323846
+#ifndef OR_W_FLOOR
+#define OR_W_FLOOR 2e-6
+#endif
 
 /* ------------------------------------------------------------------ SH
  * Real spherical harmonics with the Condon-Shortley phase, in the ordering
@@ -334,6 +337,11 @@ typedef struct {
     int contributes;     /* passes the contribution test of DESIGN.md §2 step 7 */
     uint8_t near_flags;  /* near-decision bits for this (ray, surfel) */
     double alpha, depth, val[3], ns[3];
+    /* alternatives used only by or_render_variants:
+     * the other rho3d/rho2d branch (ORF_BRANCH) and the fp32 uncertainty
+     * interval of alpha of an ill-conditioned intersection (ORF_COND) */
+    int contributes_alt;
+    double alpha_alt, depth_alt, alpha_lo, alpha_hi;
 } cand_t;
 
 static int cand_cmp(const void *pa, const void *pb) {
@@ -345,22 +353,32 @@ static int cand_cmp(const void *pa, const void *pb) {
 /* cheap per-surfel data for the result-neutral prefilter */
 typedef struct { double mus[3], c[2], reach; int culled; } pre_t;
 
-int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_t n_rays,
-              const int64_t *ray_index, double *out, uint8_t *flags, int32_t *ncontrib,
-              int nthreads) {
-    if (!sc || !se || !op || !out || sc->n < 0 || se->width < 1 || se->height < 1) return -1;
-    if (se->kind != OR_LIDAR && sc->n > 0 && !sc->sh) return -2;
-    const int cam = se->kind != OR_LIDAR;
-    const int64_t N = sc->n;
+/* one sample's ray (Eqs. 3, 5; R4) */
+typedef struct {
+    int valid;
+    uint8_t fl;           /* ray-level flags (ORF_FOV) */
+    double nu[3], nv[3], d[3], p[2], dh[3];
+} ray_t;
+
+static void make_ray(const or_sensor *se, int64_t ray, ray_t *R) {
+    const int32_t col = (int32_t)(ray % se->width), row = (int32_t)(ray / se->width);
+    R->valid = or_ray(se, col, row, R->nu, R->nv, R->d, R->p);
+    const double dn = sqrt(R->d[0] * R->d[0] + R->d[1] * R->d[1] + R->d[2] * R->d[2]);
+    for (int k = 0; k < 3; ++k) R->dh[k] = R->d[k] / dn;
+    R->fl = 0;
+    if (se->kind == OR_FISHEYE) {
+        const double mx = (R->p[0] - se->cx) / se->fx, my = (R->p[1] - se->cy) / se->fy;
+        const double tdmax = or_kb_theta_d(se->k, se->theta_max);
+        if (fabs(sqrt(mx * mx + my * my) - tdmax) < 1e-6 * tdmax) R->fl |= ORF_FOV;
+    }
+}
+
+static void prefilter_data(const or_scene *sc, const or_sensor *se, const or_opts *op, pre_t *pre) {
     const double sup = op->support_rho;
-    const double inv_s2 = 1.0 / (op->lowpass_sigma * op->lowpass_sigma);
-    pre_t *pre = (pre_t *)malloc(sizeof(pre_t) * (size_t)(N > 0 ? N : 1));
-    if (!pre) return -3;
 #ifdef _OPENMP
-    if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(static)
 #endif
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; i < sc->n; ++i) {
         centre_sensor(se, sc->means + 3 * i, pre[i].mus);
         float k = depth_key(se, pre[i].mus);
         pre[i].culled = !(k >= (float)op->near_) || !isfinite(k);
@@ -368,12 +386,176 @@ int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_
         const double su = sc->scales[2 * i], sv = sc->scales[2 * i + 1];
         pre[i].reach = 1.05 * sqrt(sup) * (su > sv ? su : sv);
     }
+}
+
+/* Evaluate surfel i on ray R (DESIGN.md §2 steps 4-7 and the §5 flags).
+ * Returns 1 and fills *c if the pair contributes or carries a flag. */
+static int eval_pair(const or_scene *sc, const or_sensor *se, const or_opts *op, const pre_t *q,
+                     int64_t i, const ray_t *R, cand_t *c) {
+    const int cam = se->kind != OR_LIDAR;
+    const double sup = op->support_rho;
+    const double inv_s2 = 1.0 / (op->lowpass_sigma * op->lowpass_sigma);
+    if (q->culled) return 0;
+    if (op->prefilter) {
+        /* exact reject: rho3d <= sup needs the hit point within
+         * sqrt(sup)*s_max of mu, i.e. the ray line within that
+         * distance of mu; rho2d <= sup needs |p-c| <= sqrt(sup)*sigma */
+        const double along = q->mus[0] * R->dh[0] + q->mus[1] * R->dh[1] + q->mus[2] * R->dh[2];
+        const double m2 = q->mus[0] * q->mus[0] + q->mus[1] * q->mus[1] + q->mus[2] * q->mus[2];
+        const double dist2 = m2 - along * along;
+        int maybe = dist2 <= q->reach * q->reach;
+        if (!maybe && cam) {
+            const double ex = R->p[0] - q->c[0], ey = R->p[1] - q->c[1];
+            const double lim = 1.05 * sqrt(sup) * op->lowpass_sigma;
+            maybe = ex * ex + ey * ey <= lim * lim;
+        }
+        if (!maybe) return 0;
+    }
+    surf_t s;
+    prep_surfel(sc, se, op, i, &s);
+    /* Eq. 2: intersect the ray's plane pair with the splat */
+    double hit[5];
+    const int h = or_intersect((const double *)s.M, R->nu, R->nv, hit);
+    const double rho3 = h ? hit[0] * hit[0] + hit[1] * hit[1] : INFINITY;
+    const double t = !h ? NAN
+                     : se->kind == OR_PINHOLE ? hit[4]
+                     : hit[2] * R->d[0] + hit[3] * R->d[1] + hit[4] * R->d[2];
+    double rho, depth, rho2 = INFINITY;
+    int use3 = 1;
+    if (cam) {   /* 2DGS low-pass floor, sigma = 1/sqrt(2) px */
+        const double ex = R->p[0] - s.c[0], ey = R->p[1] - s.c[1];
+        rho2 = (ex * ex + ey * ey) * inv_s2;
+        use3 = rho3 <= rho2;
+        rho = use3 ? rho3 : rho2;
+        depth = use3 ? t : s.cdepth;
+    } else {
+        rho = rho3;
+        depth = t;
+    }
+    const double G = exp(-0.5 * rho);
+    double alpha = s.o * G;
+    if (alpha > op->alpha_max) alpha = op->alpha_max;
+    const int contributes = rho <= sup && depth >= op->near_ && alpha >= op->alpha_min;
+    /* near-decision window: relative width
+     * w = OR_W_FLOOR + 2^-22 * cond, cond = conditioning of the
+     * intersection (u,v) w.r.t. the ray direction (3D branch
+     * only); evaluated only when a broad 1e-2 window is hit.
+     * OR_W_FLOOR = 2e-6 = 34 fp32 ulps: the fp32 evaluation error of
+     * rho, alpha and the hit depth of a well-conditioned pair is a few
+     * ulps; the cond term covers the ill-conditioned ones. */
+    uint8_t nf = 0;
+    double w = 0.0;
+    {
+        const double W0 = 1e-2;
+        const int near_any = rho <= sup * (1 + W0) && alpha >= op->alpha_min * (1 - W0) &&
+            depth >= op->near_ * (1 - W0) &&
+            (fabs(rho - sup) < sup * W0 || fabs(alpha - op->alpha_min) < op->alpha_min * W0 ||
+             fabs(depth - op->near_) < op->near_ * W0 ||
+             (cam && fabs(rho3 - rho2) < W0 * (rho3 > rho2 ? rho3 : rho2)));
+        if (near_any || (contributes && use3)) {
+            const double cj = use3 ? cond_uv((const double *)s.M, R->d) : 1.0;
+            w = OR_W_FLOOR + 2.384185791015625e-07 * cj;
+            const int okr = rho <= sup * (1 + w), oka = alpha >= op->alpha_min * (1 - w),
+                      okd = depth >= op->near_ * (1 - w);
+            if (fabs(rho - sup) < sup * w && oka && okd) nf |= ORF_SUPPORT;
+            if (fabs(alpha - op->alpha_min) < op->alpha_min * w && okr && okd) nf |= ORF_ALPHA;
+            if (fabs(depth - op->near_) < op->near_ * w && okr && oka) nf |= ORF_NEAR;
+            if (cam && okr && oka && okd && fabs(rho3 - rho2) < w * (rho3 > rho2 ? rho3 : rho2) &&
+                fabs(t - s.cdepth) > 1e-12 * fabs(s.cdepth))
+                nf |= ORF_BRANCH;
+            /* ill-conditioned intersection: an fp32 evaluation may move
+             * alpha by ~ alpha*rho*cond*2^-24; flag beyond 2.5e-5 */
+            if (contributes && use3 && alpha * (rho3 > 0.1 ? rho3 : 0.1) * cj > 419.0)
+                nf |= ORF_COND;
+        }
+    }
+    if (!(contributes || nf)) return 0;
+    memcpy(&c->key, &s.key, 4);
+    c->idx = i;
+    c->contributes = contributes;
+    c->near_flags = nf;
+    c->alpha = alpha;
+    c->depth = depth;
+    for (int k = 0; k < 3; ++k) { c->val[k] = s.val[k]; c->ns[k] = s.ns[k]; }
+    /* the other branch (ORF_BRANCH): the same tests with the other rho */
+    {
+        const double rho_a = cam ? (use3 ? rho2 : rho3) : rho;
+        const double dep_a = cam ? (use3 ? s.cdepth : t) : depth;
+        double al = s.o * exp(-0.5 * rho_a);
+        if (al > op->alpha_max) al = op->alpha_max;
+        c->alpha_alt = al;
+        c->depth_alt = dep_a;
+        c->contributes_alt = rho_a <= sup && dep_a >= op->near_ && al >= op->alpha_min;
+    }
+    /* fp32 uncertainty of alpha (ORF_COND): rho within rho +- w*max(rho,0.1),
+     * twice the predicted relative error 2*cond*2^-24 of rho3d */
+    {
+        const double e = w * (rho > 0.1 ? rho : 0.1);
+        double lo = s.o * exp(-0.5 * (rho + e)), hi = s.o * exp(-0.5 * (rho - e > 0 ? rho - e : 0.0));
+        c->alpha_lo = lo > op->alpha_max ? op->alpha_max : lo;
+        c->alpha_hi = hi > op->alpha_max ? op->alpha_max : hi;
+    }
+    return 1;
+}
+
+/* All candidates of ray R in front-to-back (key, index) order (reading R9). */
+static int64_t collect(const or_scene *sc, const or_sensor *se, const or_opts *op, const pre_t *pre,
+                       const ray_t *R, cand_t **cands, int64_t *cap) {
+    int64_t nc = 0;
+    for (int64_t i = 0; i < sc->n; ++i) {
+        if (nc == *cap) {
+            *cap *= 2;
+            cand_t *nb = (cand_t *)realloc(*cands, sizeof(cand_t) * (size_t)*cap);
+            if (!nb) return -1;
+            *cands = nb;
+        }
+        nc += eval_pair(sc, se, op, &pre[i], i, R, &(*cands)[nc]);
+    }
+    qsort(*cands, (size_t)nc, sizeof(cand_t), cand_cmp);
+    return nc;
+}
+
+/* Outputs (DESIGN.md §2 step 10) from the composite state */
+static void write_out(const or_sensor *se, const or_opts *op, int valid, double T, const double acc[3],
+                      double D, const double Nr[3], double *o) {
+    const double A = 1.0 - T;
+    if (se->kind != OR_LIDAR) {
+        if (!valid) {
+            o[0] = op->bg_rgb[0]; o[1] = op->bg_rgb[1]; o[2] = op->bg_rgb[2];
+            o[3] = 0.0; o[4] = o[5] = o[6] = 0.0; o[7] = 0.0;
+        } else {
+            for (int k = 0; k < 3; ++k) o[k] = acc[k] + T * op->bg_rgb[k];
+            o[3] = A > 0.0 ? D / A : 0.0;
+            for (int k = 0; k < 3; ++k) o[4 + k] = Nr[k];
+            o[7] = A;
+        }
+    } else {
+        o[0] = A > 0.0 ? D / A : op->bg_range;
+        o[1] = acc[0];
+        o[2] = acc[1] + T * op->bg_raydrop;
+        o[3] = A;
+        o[4] = o[5] = o[6] = o[7] = 0.0;
+    }
+}
+
+int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_t n_rays,
+              const int64_t *ray_index, double *out, uint8_t *flags, int32_t *ncontrib,
+              int nthreads) {
+    if (!sc || !se || !op || !out || sc->n < 0 || se->width < 1 || se->height < 1) return -1;
+    if (se->kind != OR_LIDAR && sc->n > 0 && !sc->sh) return -2;
+    const int64_t N = sc->n;
+    pre_t *pre = (pre_t *)malloc(sizeof(pre_t) * (size_t)(N > 0 ? N : 1));
+    if (!pre) return -3;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    prefilter_data(sc, se, op, pre);
     int err = 0;
 #ifdef _OPENMP
 #pragma omp parallel
 #endif
     {
-        int64_t cap = 1024, nc = 0;
+        int64_t cap = 1024;
         cand_t *cands = (cand_t *)malloc(sizeof(cand_t) * (size_t)cap);
         if (!cands) err = -3;
 #ifdef _OPENMP
@@ -381,110 +563,12 @@ int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_
 #endif
         for (int64_t r = 0; r < n_rays; ++r) {
             if (!cands) continue;
-            const int64_t ray = ray_index ? ray_index[r] : r;
-            const int32_t col = (int32_t)(ray % se->width), row = (int32_t)(ray / se->width);
-            double nu[3], nv[3], d[3], p[2];
-            const int valid = or_ray(se, col, row, nu, nv, d, p);
-            const double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-            const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
-            uint8_t fl = 0;
-            if (se->kind == OR_FISHEYE) {
-                const double mx = (p[0] - se->cx) / se->fx, my = (p[1] - se->cy) / se->fy;
-                const double tdmax = or_kb_theta_d(se->k, se->theta_max);
-                if (fabs(sqrt(mx * mx + my * my) - tdmax) < 1e-6 * tdmax) fl |= ORF_FOV;
-            }
-            nc = 0;
-            for (int64_t i = 0; valid && i < N; ++i) {
-                const pre_t *q = &pre[i];
-                if (q->culled) continue;
-                if (op->prefilter) {
-                    /* exact reject: rho3d <= sup needs the hit point within
-                     * sqrt(sup)*s_max of mu, i.e. the ray line within that
-                     * distance of mu; rho2d <= sup needs |p-c| <= sqrt(sup)*sigma */
-                    const double along = q->mus[0] * dh[0] + q->mus[1] * dh[1] + q->mus[2] * dh[2];
-                    const double m2 = q->mus[0] * q->mus[0] + q->mus[1] * q->mus[1] + q->mus[2] * q->mus[2];
-                    const double dist2 = m2 - along * along;
-                    int maybe = dist2 <= q->reach * q->reach;
-                    if (!maybe && cam) {
-                        const double ex = p[0] - q->c[0], ey = p[1] - q->c[1];
-                        const double lim = 1.05 * sqrt(sup) * op->lowpass_sigma;
-                        maybe = ex * ex + ey * ey <= lim * lim;
-                    }
-                    if (!maybe) continue;
-                }
-                surf_t s;
-                prep_surfel(sc, se, op, i, &s);
-                /* Eq. 2: intersect the ray's plane pair with the splat */
-                double hit[5];
-                const int h = or_intersect((const double *)s.M, nu, nv, hit);
-                const double rho3 = h ? hit[0] * hit[0] + hit[1] * hit[1] : INFINITY;
-                const double t = !h ? NAN
-                                 : se->kind == OR_PINHOLE ? hit[4]
-                                 : hit[2] * d[0] + hit[3] * d[1] + hit[4] * d[2];
-                double rho, depth, rho2 = INFINITY;
-                int use3 = 1;
-                if (cam) {   /* 2DGS low-pass floor, sigma = 1/sqrt(2) px */
-                    const double ex = p[0] - s.c[0], ey = p[1] - s.c[1];
-                    rho2 = (ex * ex + ey * ey) * inv_s2;
-                    use3 = rho3 <= rho2;
-                    rho = use3 ? rho3 : rho2;
-                    depth = use3 ? t : s.cdepth;
-                } else {
-                    rho = rho3;
-                    depth = t;
-                }
-                const double G = exp(-0.5 * rho);
-                double alpha = s.o * G;
-                if (alpha > op->alpha_max) alpha = op->alpha_max;
-                const int contributes = rho <= sup && depth >= op->near_ && alpha >= op->alpha_min;
-                /* near-decision window: relative width
-                 * w = 2e-5 + 2^-22 * cond, cond = conditioning of the
-                 * intersection (u,v) w.r.t. the ray direction (3D branch
-                 * only); evaluated only when a broad 1e-2 window is hit. */
-                uint8_t nf = 0;
-                {
-                    const double W0 = 1e-2;
-                    const int near_any = rho <= sup * (1 + W0) && alpha >= op->alpha_min * (1 - W0) &&
-                        depth >= op->near_ * (1 - W0) &&
-                        (fabs(rho - sup) < sup * W0 || fabs(alpha - op->alpha_min) < op->alpha_min * W0 ||
-                         fabs(depth - op->near_) < op->near_ * W0 ||
-                         (cam && fabs(rho3 - rho2) < W0 * (rho3 > rho2 ? rho3 : rho2)));
-                    if (near_any || (contributes && use3)) {
-                        const double cj = use3 ? cond_uv((const double *)s.M, d) : 1.0;
-                        const double w = 2e-5 + 2.384185791015625e-07 * cj;
-                        const int okr = rho <= sup * (1 + w), oka = alpha >= op->alpha_min * (1 - w),
-                                  okd = depth >= op->near_ * (1 - w);
-                        if (fabs(rho - sup) < sup * w && oka && okd) nf |= ORF_SUPPORT;
-                        if (fabs(alpha - op->alpha_min) < op->alpha_min * w && okr && okd) nf |= ORF_ALPHA;
-                        if (fabs(depth - op->near_) < op->near_ * w && okr && oka) nf |= ORF_NEAR;
-                        if (cam && okr && oka && okd && fabs(rho3 - rho2) < w * (rho3 > rho2 ? rho3 : rho2) &&
-                            fabs(t - s.cdepth) > 1e-12 * fabs(s.cdepth))
-                            nf |= ORF_BRANCH;
-                        /* ill-conditioned intersection: an fp32 evaluation may move
-                         * alpha by ~ alpha*rho*cond*2^-24; flag beyond 2.5e-5 */
-                        if (contributes && use3 && alpha * (rho3 > 0.1 ? rho3 : 0.1) * cj > 419.0)
-                            nf |= ORF_COND;
-                    }
-                }
-                if (contributes || nf) {
-                    if (nc == cap) {
-                        cap *= 2;
-                        cand_t *nb = (cand_t *)realloc(cands, sizeof(cand_t) * (size_t)cap);
-                        if (!nb) { err = -3; break; }
-                        cands = nb;
-                    }
-                    cand_t *c = &cands[nc++];
-                    memcpy(&c->key, &s.key, 4);
-                    c->idx = i;
-                    c->contributes = contributes;
-                    c->near_flags = nf;
-                    c->alpha = alpha;
-                    c->depth = depth;
-                    for (int k = 0; k < 3; ++k) { c->val[k] = s.val[k]; c->ns[k] = s.ns[k]; }
-                }
-            }
-            /* front-to-back in (key, index) order (reading R9) */
-            qsort(cands, (size_t)nc, sizeof(cand_t), cand_cmp);
+            ray_t R;
+            make_ray(se, ray_index ? ray_index[r] : r, &R);
+            uint8_t fl = R.fl;
+            const int64_t nc = R.valid ? collect(sc, se, op, pre, &R, &cands, &cap) : 0;
+            if (nc < 0) { err = -3; continue; }
+            /* front-to-back composite (north_star; DESIGN.md §2 step 9) */
             double T = 1.0, acc[3] = {0, 0, 0}, D = 0.0, Nr[3] = {0, 0, 0};
             int32_t used = 0;
             for (int64_t j = 0; j < nc; ++j) {
@@ -500,25 +584,7 @@ int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_
                 T = Tn;
                 ++used;
             }
-            double *o = out + 8 * r;
-            const double A = 1.0 - T;
-            if (cam) {
-                if (!valid) {
-                    o[0] = op->bg_rgb[0]; o[1] = op->bg_rgb[1]; o[2] = op->bg_rgb[2];
-                    o[3] = 0.0; o[4] = o[5] = o[6] = 0.0; o[7] = 0.0;
-                } else {
-                    for (int k = 0; k < 3; ++k) o[k] = acc[k] + T * op->bg_rgb[k];
-                    o[3] = A > 0.0 ? D / A : 0.0;
-                    for (int k = 0; k < 3; ++k) o[4 + k] = Nr[k];
-                    o[7] = A;
-                }
-            } else {
-                o[0] = A > 0.0 ? D / A : op->bg_range;
-                o[1] = acc[0];
-                o[2] = acc[1] + T * op->bg_raydrop;
-                o[3] = A;
-                o[4] = o[5] = o[6] = o[7] = 0.0;
-            }
+            write_out(se, op, R.valid, T, acc, D, Nr, out + 8 * r);
             if (flags) flags[r] = fl;
             if (ncontrib) ncontrib[r] = used;
         }
@@ -527,3 +593,152 @@ int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_
     free(pre);
     return err;
 }
+
+/* ------------------------------------------------- near-decision variants
+ * DESIGN.md §5 (strict two-sided gate for flagged rays).  A flagged ray's
+ * result is not unique in fp32: each near decision may fall either way and an
+ * ill-conditioned intersection leaves alpha uncertain within an interval.
+ * The variants are every composite the definition gives when each flagged
+ * (ray, surfel) pair takes each of its admissible states:
+ *   SUPPORT/ALPHA/NEAR  contributes or not;
+ *   BRANCH              the rho3d or the rho2d branch (each with its own tests);
+ *   COND                alpha nominal or at either end of its interval;
+ *   TSTOP               a step whose T(1-alpha) is within 1e-4 relative of
+ *                       t_min stops or composites;
+ *   FOV                 the fisheye sample is inside or outside the FOV.
+ * Variant 0 is always the nominal composite (the one or_render returns). */
+typedef struct {
+    const or_sensor *se;
+    const or_opts *op;
+    const cand_t *c;
+    int64_t nc;
+    int valid;
+    int32_t max_var, count;
+    double *out;          /* [max_var, 8] */
+    uint8_t seen;         /* union of flags met on any variant path */
+} var_ctx;
+
+typedef struct { int contributes; double alpha, depth; } state_t;
+
+/* admissible states of a flagged pair; state 0 is the nominal one */
+static int cand_states(const cand_t *c, state_t st[8]) {
+    int n = 0;
+    const uint8_t f = c->near_flags;
+    const int dec = (f & (ORF_SUPPORT | ORF_ALPHA | ORF_NEAR)) != 0;
+    for (int b = 0; b < ((f & ORF_BRANCH) ? 2 : 1); ++b) {
+        const double al = b ? c->alpha_alt : c->alpha, dp = b ? c->depth_alt : c->depth;
+        const int con = b ? c->contributes_alt : c->contributes;
+        for (int t = 0; t < (dec ? 2 : 1); ++t) {
+            const int cc = t ? !con : con;
+            st[n++] = (state_t){cc, al, dp};
+            if (cc && !b && (f & ORF_COND)) {
+                st[n++] = (state_t){1, c->alpha_lo, dp};
+                st[n++] = (state_t){1, c->alpha_hi, dp};
+            }
+        }
+    }
+    return n;
+}
+
+/* Composite candidates j.. from state (T, acc, D, Nr); branch at every
+ * flagged pair and every near-t_min stop; write one output per leaf. */
+static void var_walk(var_ctx *x, int64_t j, double T, const double acc0[3], double D,
+                     const double Nr0[3]) {
+    double acc[3] = {acc0[0], acc0[1], acc0[2]}, Nr[3] = {Nr0[0], Nr0[1], Nr0[2]};
+    const double tmin = x->op->t_min;
+    for (; j < x->nc; ++j) {
+        if (x->count > x->max_var) return;
+        const cand_t *c = &x->c[j];
+        x->seen |= c->near_flags;
+        state_t st[8];
+        const int ns = c->near_flags ? cand_states(c, st) : 1;
+        if (!c->near_flags) st[0] = (state_t){c->contributes, c->alpha, c->depth};
+        for (int k = 0; k < ns; ++k) {
+            const state_t s = st[k];
+            if (!s.contributes) {
+                if (ns == 1) goto next;
+                var_walk(x, j + 1, T, acc, D, Nr);
+                continue;
+            }
+            const double Tn = T * (1.0 - s.alpha);
+            const int near_stop = fabs(Tn - tmin) < tmin * 1e-4;
+            if (near_stop) x->seen |= ORF_TSTOP;
+            if (ns == 1 && !near_stop) {
+                if (Tn < tmin) goto done;   /* stop; not composited (R3) */
+                const double wgt = s.alpha * T;
+                for (int q = 0; q < 3; ++q) { acc[q] += wgt * c->val[q]; Nr[q] += wgt * c->ns[q]; }
+                D += wgt * s.depth;
+                T = Tn;
+                goto next;
+            }
+            /* the nominal decision first, then (near t_min) the other one */
+            for (int o = 0; o < (near_stop ? 2 : 1); ++o) {
+                const int stop = o ? !(Tn < tmin) : (Tn < tmin);
+                if (stop) {
+                    var_walk(x, x->nc, T, acc, D, Nr);
+                } else {
+                    const double wgt = s.alpha * T;
+                    double a3[3], N3[3];
+                    for (int q = 0; q < 3; ++q) { a3[q] = acc[q] + wgt * c->val[q]; N3[q] = Nr[q] + wgt * c->ns[q]; }
+                    var_walk(x, j + 1, Tn, a3, D + wgt * s.depth, N3);
+                }
+            }
+        }
+        return;
+    next:;
+    }
+done:
+    if (x->count < x->max_var) write_out(x->se, x->op, x->valid, T, acc, D, Nr, x->out + 8 * x->count);
+    x->count++;
+}
+
+int or_render_variants(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_t n_rays,
+                       const int64_t *ray_index, int32_t max_var, double *var_out, int32_t *nvar,
+                       uint8_t *seen, int nthreads) {
+    if (!sc || !se || !op || !var_out || !nvar || sc->n < 0 || max_var < 1 || se->width < 1 ||
+        se->height < 1)
+        return -1;
+    if (se->kind != OR_LIDAR && sc->n > 0 && !sc->sh) return -2;
+    const int64_t N = sc->n;
+    pre_t *pre = (pre_t *)malloc(sizeof(pre_t) * (size_t)(N > 0 ? N : 1));
+    if (!pre) return -3;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    prefilter_data(sc, se, op, pre);
+    int err = 0;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+    {
+        int64_t cap = 1024;
+        cand_t *cands = (cand_t *)malloc(sizeof(cand_t) * (size_t)cap);
+        if (!cands) err = -3;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int64_t r = 0; r < n_rays; ++r) {
+            if (!cands) continue;
+            ray_t R;
+            make_ray(se, ray_index ? ray_index[r] : r, &R);
+            /* a FOV-edge sample also gets the variants of the other side */
+            const int64_t nc = (R.valid || (R.fl & ORF_FOV)) ? collect(sc, se, op, pre, &R, &cands, &cap) : 0;
+            if (nc < 0) { err = -3; continue; }
+            var_ctx x = {se, op, cands, nc, R.valid, max_var, 0, var_out + (size_t)8 * max_var * r, R.fl};
+            const double z3[3] = {0, 0, 0};
+            var_walk(&x, 0, 1.0, z3, 0.0, z3);
+            if (R.fl & ORF_FOV) {
+                x.valid = !R.valid;
+                var_walk(&x, 0, 1.0, z3, 0.0, z3);
+            }
+            nvar[r] = x.count;
+            if (seen) seen[r] = x.seen;
+        }
+        free(cands);
+    }
+    free(pre);
+    return err;
+}
+
+/* Conditioning of the intersection (exported for the flag-logic pins). */
+double or_cond_uv(const double M[9], const double d[3]) { return cond_uv(M, d); }

@@ -63,6 +63,22 @@ int or_render(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_
               const int64_t *ray_index, double *out, uint8_t *flags, int32_t *ncontrib,
               int nthreads);
 
+/* Near-decision variants of each ray (DESIGN.md §5 strict two-sided gate):
+ * every composite the definition gives when each flagged (ray, surfel) pair
+ * takes each admissible state (decision either way, the other rho branch,
+ * alpha at the ends of its fp32 interval, a near-t_min stop either way, a
+ * FOV-edge sample either side).  var_out: [n_rays, max_var, 8], variant 0 is
+ * the nominal composite; nvar[r] = number of variants (> max_var: only the
+ * first max_var were written, the ray is unresolved); seen[r] (may be NULL) =
+ * union of the flags met on any variant path. */
+int or_render_variants(const or_scene *sc, const or_sensor *se, const or_opts *op, int64_t n_rays,
+                       const int64_t *ray_index, int32_t max_var, double *var_out, int32_t *nvar,
+                       uint8_t *seen, int nthreads);
+
+/* sigma_max / sigma_min of d(u,v)/d(ray tangent angles) at direction d for
+ * the splat M (row-major, sensor frame): the conditioning used by the flags. */
+double or_cond_uv(const double M[9], const double d[3]);
+
 /* Per-surfel sort key (reading R9): fp32 bits of the pinned fp64
  * depth, and the cull flag (key < near or non-finite). */
 int or_keys(const or_scene *sc, const or_sensor *se, const or_opts *op, uint32_t *key_bits,
