@@ -358,3 +358,60 @@ def chunked(n_chunks: int = 8, per_chunk: int = 1_500_000, timesteps: int = CHUN
 def make_config(name: str, **kw) -> Config:
     return {"tiny": tiny, "mid": mid, "fisheye": fisheye_cfg, "lidar": lidar_cfg,
             "chunked": chunked}[name](**kw)
+
+
+# --------------------------------------------------------------------------- neural Gaussians (NEXT-1)
+@dataclass
+class Anchors:
+    """Scaffold-style anchors (DESIGN.md §12 reading N1): position [n,3] f32,
+    feature [n,32] f16, base_scale [n,3] f32."""
+    position: np.ndarray
+    feature: np.ndarray
+    base_scale: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return int(self.position.shape[0])
+
+
+NEURAL_K, NEURAL_F, NEURAL_H = 5, 32, 32
+NEURAL_OUT = {"offset": 15, "scale": 10, "rotation": 30, "opacity": 5, "color": 15, "intensity": 5,
+              "raydrop": 5}
+NEURAL_CAMERA_HEADS = ("offset", "scale", "rotation", "opacity", "color")
+NEURAL_LIDAR_HEADS = ("offset", "scale", "rotation", "opacity", "intensity", "raydrop")
+
+
+def street_anchors(rng, n: int, z0: float, z1: float, s_lo=0.03, s_hi=0.2) -> Anchors:
+    """Anchors on the synthetic street surfaces (positions as in `street`),
+    features ~ N(0,1) stored fp16, isotropic base scale log-U[s_lo, s_hi]."""
+    pos = street(rng, n, z0, z1, 0, with_sh=False).means
+    feat = rng.normal(0.0, 1.0, (n, NEURAL_F)).astype(np.float16)
+    l = np.exp(rng.uniform(np.log(s_lo), np.log(s_hi), n))
+    base = np.repeat(l[:, None], 3, axis=1).astype(np.float32)
+    return Anchors(np.ascontiguousarray(pos, np.float32), np.ascontiguousarray(feat), base)
+
+
+def neural_decoder(rng, modality: str = "camera") -> dict:
+    """Random-init decoder (no trained weights exist here): per head
+    W1 [32,in] (in = 32 geometry heads, 35 appearance heads), W2 [32,32],
+    W3 [out,32] ~ N(0, 1/fan_in) stored fp16; biases ~ N(0, 0.1) fp32, with
+    the rotation head's output bias set to the identity 6D frame (1,0,0,0,1,0)
+    per surfel and the opacity bias raised by 1 (mostly opaque surfels)."""
+    heads = NEURAL_CAMERA_HEADS if modality == "camera" else NEURAL_LIDAR_HEADS
+    dec = {}
+    for h in heads:
+        nin = NEURAL_F if h in ("offset", "scale", "rotation") else NEURAL_F + 3
+        out = NEURAL_OUT[h]
+        W1 = rng.normal(0.0, 1.0 / math.sqrt(nin), (NEURAL_H, nin))
+        W2 = rng.normal(0.0, 1.0 / math.sqrt(NEURAL_H), (NEURAL_H, NEURAL_H))
+        W3 = rng.normal(0.0, 0.5 / math.sqrt(NEURAL_H), (out, NEURAL_H))
+        b1 = rng.normal(0.0, 0.1, NEURAL_H)
+        b2 = rng.normal(0.0, 0.1, NEURAL_H)
+        b3 = rng.normal(0.0, 0.1, out)
+        if h == "rotation":
+            b3 += np.tile([1.0, 0.0, 0.0, 0.0, 1.0, 0.0], NEURAL_K)
+        if h == "opacity":
+            b3 += 1.0
+        dec[h] = {"W1": W1.astype(np.float16), "b1": b1.astype(np.float32), "W2": W2.astype(np.float16),
+                  "b2": b2.astype(np.float32), "W3": W3.astype(np.float16), "b3": b3.astype(np.float32)}
+    return dec
