@@ -130,21 +130,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
-def oracle_rate(surfels, sensors, n_rays, seed, cores, frames_per_sample=4):
+def oracle_rate(surfels, sensors, n_rays, seed, cores, frames_per_sample=4, keep=None):
     """Time the fp64 oracle on n_rays random rays of random frames of the
-    batch.  Returns (rays/s, rays, seconds)."""
+    batch.  Returns (rays/s, rays, seconds); keep (a list), if given, receives
+    (frame index, rays, oracle output, flags) per frame."""
     import oracle
     rng = np.random.default_rng(seed)
     fr = rng.choice(len(sensors), size=min(frames_per_sample, len(sensors)), replace=False)
     per = max(1, n_rays // len(fr))
-    t0 = time.perf_counter()
+    dt = 0.0
     done = 0
     for f in fr:
         se = sensors[int(f)]
-        rays = rng.choice(se.width * se.height, size=min(per, se.width * se.height), replace=False)
-        oracle.render(surfels, se, rays, nthreads=cores)
+        rays = np.sort(rng.choice(se.width * se.height, size=min(per, se.width * se.height), replace=False))
+        t0 = time.perf_counter()
+        ref, fl, _ = oracle.render(surfels, se, rays, nthreads=cores)
+        dt += time.perf_counter() - t0
         done += len(rays)
-    dt = time.perf_counter() - t0
+        if keep is not None:
+            keep.append((int(f), rays, ref, fl))
     return done / dt, done, dt
 
 
@@ -152,14 +156,39 @@ def cpu_cores():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_baseline(surfels, sensors, target_s=15.0):
+def cpu_baseline(surfels, sensors, target_s=15.0, gpu_frames=None):
+    """The oracle timed on a bounded random-ray sample of the batch.  With
+    gpu_frames (frame index -> the GPU's rendered [C,H,W] tensor) the same
+    oracle rays also give the parity spot check of the bench line (the strict
+    gate of tests/parity.py; full-frame statistics: profiles/parity_r02.json)."""
     cores = cpu_cores()
     r0, n0, t0 = oracle_rate(surfels, sensors, 64, 1234, cores, 1)   # calibration
     n = int(min(20000, max(64, r0 * target_s)))
-    r, n, t = oracle_rate(surfels, sensors, n, 4321, cores)
-    return {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} random rays over 4 random frames of the batch ({t:.1f} s of CPU work, "
-                      f"fp64 brute force over all {surfels.n} surfels per ray, OpenMP {cores} threads)"}
+    keep = []
+    r, n, t = oracle_rate(surfels, sensors, n, 4321, cores, keep=keep)
+    cpu = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{n} random rays over 4 random frames of the batch ({t:.1f} s of CPU work, "
+                     f"fp64 brute force over all {surfels.n} surfels per ray, OpenMP {cores} threads)"}
+    par = None
+    if gpu_frames is not None:
+        from tests import parity
+        agg = dict(rays=0, flagged=0, ambiguous=0, bad=0, bad_flagged=0, unresolved=0, max_abs=0.0,
+                   max_rel_depth=0.0, frames=[])
+        for f, rays, ref, fl in keep:
+            st = parity.compare(gpu_frames(f), ref, fl, rays, sensors[f], surfels)
+            agg["rays"] += st["n"]
+            for k in ("flagged", "ambiguous", "bad", "bad_flagged", "unresolved"):
+                agg[k] += st[k]
+            agg["max_abs"] = max(agg["max_abs"], st["max_abs_unflagged"])
+            agg["max_rel_depth"] = max(agg["max_rel_depth"], st["max_rel_depth_unflagged"])
+            agg["frames"].append(f)
+        agg["ok"] = (agg["bad"] == 0 and agg["bad_flagged"] == 0 and agg["unresolved"] == 0 and
+                     agg["ambiguous"] <= max(2, parity.MAX_AMBIGUOUS_FRAC * agg["rays"]))
+        agg["gate"] = ("tests/parity.py: 1e-4 abs (rgb/alpha/normal/intensity/raydrop), 1e-4 rel (depth/range) "
+                       "on every ray; flagged rays against the oracle's near-decision variants")
+        agg["full_frames"] = "profiles/parity_r02.json"
+        par = agg
+    return cpu, par
 
 
 def run_reference(args):
@@ -270,71 +299,37 @@ def run_gsr(args):
     caps, contrib, evals = br.plan(my_sensors, stats=True)
     sensors = br.wrap(my_sensors)
 
-    # output slabs per sensor kind, batch order; rank 0 holds the whole batch
+    # output slabs per sensor kind in batch order (rank 0 holds the whole batch), the
+    # per-frame output views and the gather to rank 0: dist.ShardedBatch
     def kind_frames(ss, k):
         return [i for i, s in enumerate(ss) if int(s.kind) == k]
-    slabs_full, slabs_local, outs = {}, {}, [None] * len(sensors)
-    for k in kinds:
-        ref = next(s for s in all_sensors if int(s.kind) == k)
-        C = 4 if k == gsr.GS_LIDAR_SPINNING else 8
-        per_t = sum(1 for s in groups[0] if int(s.kind) == k)
-        n_all = per_t * n_steps_t
-        idx = kind_frames(my_sensors, k)
-        if rank == 0:
-            slabs_full[k] = torch.empty((n_all, C, ref.height, ref.width), dtype=torch.float32, device=device)
-            slabs_local[k] = slabs_full[k][per_t * lo: per_t * hi]
-        else:
-            slabs_local[k] = torch.empty((len(idx), C, ref.height, ref.width), dtype=torch.float32, device=device)
-        for j, i in enumerate(idx):
-            outs[i] = slabs_local[k][j]
-
-    def gather():
-        reqs = []
-        for k in kinds:
-            per_t = sum(1 for s in groups[0] if int(s.kind) == k)
-            full = slabs_full.get(k)
-            # blocks of timesteps -> blocks of frames of this kind
-            loc = slabs_local[k]
-            if world > 1:
-                fv = full.view(n_steps_t, per_t, *full.shape[1:]) if full is not None else None
-                lv = loc.view(hi - lo, per_t, *loc.shape[1:])
-                reqs += gd.gather_blocks(lv, fv, n_steps_t, world, rank)
-        for r in reqs:
-            r.wait()
-
-    per_step_t = len(groups[0])
+    specs = [(int(s.kind), 4 if int(s.kind) == gsr.GS_LIDAR_SPINNING else 8, s.height, s.width) for s in groups[0]]
+    sb = gd.ShardedBatch(specs, n_steps_t, world, rank, device)
+    assert len(sb.outs) == len(sensors)
+    outs, slabs_full, slabs_local = sb.outs, sb.full, sb.local
+    gather = sb.gather
+    per_step_t = sb.frames_per_timestep
     cur = torch.cuda.current_stream(device)
     comm = torch.cuda.Stream(device) if world > 1 else None
-    local_blocks = {k: slabs_local[k].view(hi - lo, sum(1 for s in groups[0] if int(s.kind) == k),
-                                           *slabs_local[k].shape[1:]) for k in kinds}
-    full_blocks = ({k: slabs_full[k].view(n_steps_t, sum(1 for s in groups[0] if int(s.kind) == k),
-                                          *slabs_full[k].shape[1:]) for k in kinds} if rank == 0 else None)
 
     def step(times=None, on_frame=None, event_log=None):
         if world > 1 and args.gather == "rounds":
             # post gather round j (this rank's j-th timestep) as soon as its frames are enqueued
             reqs = []
-            import torch.distributed as dist
 
             def post(i, st):
                 if on_frame is not None:
                     on_frame(i, st)
                 if i % per_step_t != per_step_t - 1:
                     return
-                j = i // per_step_t
                 for lane_st in br.streams:
                     comm.wait_stream(lane_st)
-                ops = gd.round_ops(local_blocks, full_blocks, j, n_steps_t, world, rank)
                 with torch.cuda.stream(comm):
-                    if ops:
-                        reqs.extend(dist.batch_isend_irecv(ops))
+                    reqs.extend(sb.round(i // per_step_t))
             br.render(sensors, outs, times=times, on_frame=post, event_log=event_log)
-            if rank == 0:   # rounds the root has no timestep for (uneven blocks) still receive
-                for j in range(hi - lo, gd.n_rounds(n_steps_t, world)):
-                    ops = gd.round_ops(local_blocks, full_blocks, j, n_steps_t, world, rank)
-                    with torch.cuda.stream(comm):
-                        if ops:
-                            reqs.extend(dist.batch_isend_irecv(ops))
+            for j in sb.rounds_left():   # rounds the root has no timestep for (uneven blocks)
+                with torch.cuda.stream(comm):
+                    reqs.extend(sb.round(j))
             for r in reqs:
                 r.wait()
             cur.wait_stream(comm)
@@ -342,15 +337,34 @@ def run_gsr(args):
         br.render(sensors, outs, times=times, on_frame=on_frame, event_log=event_log)
         gather()
 
+    n0 = gsr.gs_kernel_launches()
+    step()   # one eager step: the library's launch count per step (a replay launches the same kernels)
+    torch.cuda.synchronize(device)
+    launches_per_step = gsr.gs_kernel_launches() - n0
+    graph_note = None
+    # one CUDA graph for the whole local batch (capacity mode: no host sync inside):
+    # a replay enqueues every frame's ~20 library launches with one host call
+    graph = None
+    if args.graph and not (world > 1 and args.gather == "rounds"):
+        graph = br.capture(sensors, outs)
+        graph_note = "each step is one replay of a CUDA graph of the whole local batch (all frames, all streams)"
+
+    def step_graph():
+        graph.replay()
+        gather()
+
+    run_step = step_graph if graph is not None else step
     for _ in range(args.warmup):
-        step()
+        run_step()
     torch.cuda.synchronize(device)
     ovf = br.overflowed()
     assert not ovf, f"pair capacity exceeded on frames {ovf}"
+    nccl = None
+    if world > 1 and rank == 0:
+        nccl = gd.nccl_init_info()
 
     # ---------------- timed region (device-resident inputs)
     sampler = ClockSampler(list(range(world))).start() if rank == 0 else None
-    event_log = []   # per-frame events of the timed steps (read after the final sync)
     n_launch0 = gsr.gs_kernel_launches()
     gd.barrier(world, device)
     torch.cuda.synchronize(device)
@@ -360,20 +374,29 @@ def run_gsr(args):
     t_all0.record(cur)
     th0 = time.perf_counter()
     for _ in range(args.steps):
-        step(event_log=event_log)
+        run_step()
     t_all1.record(cur)
     host_enqueue_ms = (time.perf_counter() - th0) * 1e3 / args.steps   # host time to enqueue a step
     torch.cuda.synchronize(device)
     gd.barrier(world, device)
     n_launch = gsr.gs_kernel_launches() - n_launch0
+    if graph is not None:   # the library's counter only sees the capture: replays launch the same kernels
+        n_launch = launches_per_step * args.steps
     clocks = sampler.stop() if sampler else None
+    assert not br.overflowed()
     ms_local = t_all0.elapsed_time(t_all1) / args.steps
     ms_step = gd.max_over_ranks(ms_local, device, world)
     total_samples = samples_of(all_sensors)
     value = total_samples / (ms_step * 1e-3) / 1e6
+    cam_px = sum(int(s.width) * int(s.height) for s in all_sensors if int(s.kind) != gsr.GS_LIDAR_SPINNING)
+    lid_rays = total_samples - cam_px
 
-    # ---------------- per-entry-point durations: CUDA events recorded on each frame's stream
-    # during the timed steps (with 4 streams they include overlap with other frames)
+    # ---------------- per-entry-point durations (context): one eager step after the timed
+    # region with CUDA events on each frame's stream (streams overlap, so they include
+    # other frames' kernels)
+    event_log = []
+    step(event_log=event_log)
+    torch.cuda.synchronize(device)
     times = FrameTimes.from_events(event_log)
     nf = len(sensors)
     reps = len(times.render) // nf
@@ -396,7 +419,7 @@ def run_gsr(args):
     instr = float(np.mean([contrib[i] for i in idx])) * INSTR_PER_PAIR[dom_kind]
     clk = (clocks or {}).get("sm_max_mhz") or 1965.0
     peak = SM_COUNT * FP32_LANES * clk * 1e6 / 1e12
-    achieved = instr / t_render / 1e12 if t_render > 0 else 0.0
+    achieved_span = instr / t_render / 1e12 if t_render > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -404,7 +427,8 @@ def run_gsr(args):
             traffic = json.load(open(tp)).get(f"{args.workload}:{dom_kind}")
         except (OSError, ValueError):
             traffic = None
-    # context: the same launches one at a time on one stream (no overlap), a sample of frames
+    # the kernel's own time: the same launches one at a time on one stream with the full
+    # grid (no overlap), a sample of frames, CUDA events on that stream
     iso_idx = [i for i in idx if (i // 7) % 8 == 0] or idx
     lane = br.lanes[0]
     iso_ev = []
@@ -419,20 +443,19 @@ def run_gsr(args):
     t_iso = float(np.mean([ev[2].elapsed_time(ev[3]) for ev in iso_ev])) * 1e-3
     instr_iso = float(np.mean([contrib[i] for i in iso_idx])) * INSTR_PER_PAIR[dom_kind]
     roofline = {"kernel": f"gs_render_camera ({'pinhole' if dom_kind == 0 else 'kind %d' % dom_kind})",
-                "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 2), "unit": "Tinst/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "bound": "alu", "achieved": round(instr_iso / t_iso / 1e12, 4), "peak": round(peak, 2),
+                "unit": "Tinst/s", "frac": round(instr_iso / t_iso / 1e12 / peak, 4), "traffic": traffic,
                 "work": f"{INSTR_PER_PAIR[dom_kind]} FP32 lane-instr x composited pairs per launch "
-                        f"(mean {int(np.mean([contrib[i] for i in idx]))}), peak = {SM_COUNT} SMs x {FP32_LANES} "
-                        f"FP32 lanes x {clk:.0f} MHz (sm_max)",
-                "ms_per_launch": round(t_render * 1e3, 4),
-                "note": f"timed-region events: {args.streams} streams overlap and each compositing grid takes "
-                        f"grid_share={lane.cam_opts.grid_share:.3g} of the GPU, so one launch's event span "
-                        f"includes other frames' kernels; see 'isolated' for the kernel alone",
-                "isolated": {"ms_per_launch": round(t_iso * 1e3, 4),
-                             "achieved": round(instr_iso / t_iso / 1e12, 4),
-                             "frac": round(instr_iso / t_iso / 1e12 / peak, 4),
-                             "note": f"{len(iso_idx)} camera frames re-rendered one at a time on one stream "
-                                     f"(full grid) right after the timed region, CUDA events on that stream"},
+                        f"(mean {int(np.mean([contrib[i] for i in iso_idx]))} over {len(iso_idx)} frames), "
+                        f"peak = {SM_COUNT} SMs x {FP32_LANES} FP32 lanes x {clk:.0f} MHz (sm_max)",
+                "ms_per_launch": round(t_iso * 1e3, 4),
+                "how": f"the kernel's own time: {len(iso_idx)} camera frames of the batch re-rendered one at a "
+                       "time on one stream with the full grid right after the timed region, CUDA events on "
+                       "that stream around the gs_render_camera call",
+                "in_step": {"ms_event_span": round(t_render * 1e3, 4), "achieved": round(achieved_span, 4),
+                            "note": f"inside a step {args.streams} streams overlap and each compositing grid "
+                                    f"takes grid_share={lane.cam_opts.grid_share:.3g} of the GPU, so one "
+                                    "launch's event span includes other frames' kernels"},
                 "step_aggregate": {"achieved": round(instr * len(idx) / (ms_step * 1e-3) / 1e12, 4),
                                    "frac": round(instr * len(idx) / (ms_step * 1e-3) / 1e12 / peak, 4),
                                    "note": "all composited work of this kind in a step / the step time "
@@ -443,13 +466,16 @@ def run_gsr(args):
     if not args.no_e2e:
         host = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in surf.items()}
         h2d = sum(v.numel() * v.element_size() for v in host.values() if isinstance(v, torch.Tensor))
-        host_out = {k: torch.empty(slabs_local[k].shape, dtype=torch.float32, pin_memory=True) for k in kinds}
-        host_views = [None] * len(sensors)
-        for k in kinds:
-            for j, i in enumerate(kind_frames(my_sensors, k)):
-                host_views[i] = host_out[k][j]
+        # rank 0 receives the whole gathered batch into pinned host memory
+        host_src = slabs_full if rank == 0 else {}
+        host_out = {k: torch.empty(t.shape, dtype=torch.float32, pin_memory=True) for k, t in host_src.items()}
         d2h = sum(t.numel() * 4 for t in host_out.values())
         copy_stream = torch.cuda.Stream(device)
+        host_views = [None] * len(sensors)
+        if world == 1:   # frame-by-frame copies overlap the following frames
+            for k in kinds:
+                for j, i in enumerate(kind_frames(my_sensors, k)):
+                    host_views[i] = host_out[k][j]
 
         def on_frame(i, st):
             ev = torch.cuda.Event()
@@ -464,6 +490,13 @@ def run_gsr(args):
         dev2 = [surf, {k: (torch.empty_like(v) if isinstance(v, torch.Tensor) else v) for k, v in surf.items()}]
         up_stream = torch.cuda.Stream(device)
         up_done, used = [None, None], [None, None]
+        graphs2 = [None, None]
+        if graph is not None:
+            for bi in (0, 1):
+                br.set_surfels(dev2[bi])
+                graphs2[bi] = br.capture(sensors, outs, on_frame=on_frame if world == 1 else None,
+                                         join=(copy_stream,) if world == 1 else ())
+            del graph
 
         def upload(j):
             bi = j % 2
@@ -481,10 +514,20 @@ def run_gsr(args):
             if j == 0:
                 upload(0)
             cur.wait_event(up_done[bi])
-            br.set_surfels(dev2[bi])
             if not last:
                 upload(j + 1)
-            br.render(sensors, outs, on_frame=on_frame)
+            if graphs2[bi] is not None:
+                graphs2[bi].replay()
+            else:
+                br.set_surfels(dev2[bi])
+                br.render(sensors, outs, on_frame=on_frame if world == 1 else None)
+            if world > 1:
+                gather()   # NCCL p2p gather of every frame to rank 0 ...
+                if rank == 0:   # ... and rank 0's copy of the whole batch to host
+                    copy_stream.wait_stream(cur)
+                    with torch.cuda.stream(copy_stream):
+                        for k in kinds:
+                            host_out[k].copy_(slabs_full[k], non_blocking=True)
             cur.wait_stream(copy_stream)
             used[bi] = torch.cuda.Event()
             used[bi].record(cur)
@@ -502,15 +545,21 @@ def run_gsr(args):
         gd.barrier(world, device)
         ms_e2e = gd.max_over_ranks(a.elapsed_time(b) / args.steps, device, world)
         assert not br.overflowed()
-        e2e = {"value": total_samples / (ms_e2e * 1e-3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms_e2e, 3),
+        e2e = {"value": round(total_samples / (ms_e2e * 1e-3) / 1e6, 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms_e2e, 3),
+               "camera_Mpixel_s": round(cam_px / (ms_e2e * 1e-3) / 1e6, 2),
+               "lidar_Mrays_s": round(lid_rays / (ms_e2e * 1e-3) / 1e6, 2),
                "path": "pinned host surfels -> device (double-buffered: step j+1's upload overlaps step j), "
-                       "BatchRenderer (C-ABI), every frame -> pinned host on a copy stream overlapping the next "
-                       "frames; per rank, no gather"}
+                       "BatchRenderer (C-ABI%s), %s" % (
+                           ", one CUDA graph per surfel buffer" if graphs2[0] is not None else "",
+                           "every frame -> pinned host on a copy stream overlapping the next frames"
+                           if world == 1 else "NCCL p2p gather of every frame to rank 0, then rank 0 copies "
+                                              "the whole batch to pinned host (bytes counted on rank 0)")}
 
-    cpu = None
+    cpu, par = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(surfels_np, all_sensors, args.cpu_seconds)
+        cpu, par = cpu_baseline(surfels_np, all_sensors, args.cpu_seconds,
+                                gpu_frames=lambda f: outs[f].cpu().numpy())
     per_config = None
     if rank == 0 and not args.no_configs:
         per_config = measure_configs(device)
@@ -518,6 +567,7 @@ def run_gsr(args):
     if rank == 0:
         desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
                     if world > 1 else "1 GPU", streams=args.streams, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
+                    cuda_graph=graph_note,
                     l2="no flush: resident surfels (%.2f GB) and outputs (%.1f GB) exceed the 126 MB L2" % (
                         sum(v.numel() * 4 for v in surf.values() if isinstance(v, torch.Tensor)) / 1e9,
                         sum(t.numel() * 4 for t in slabs_full.values()) / 1e9))
@@ -525,10 +575,12 @@ def run_gsr(args):
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenegen seeds, "
                 "BASELINE.json configs; random surfels, no trained scene)", "config": desc,
-                "e2e": e2e, "gpu_launches": int(n_launch), "gpu_launches_per_step": n_launch // args.steps,
+                "camera_Mpixel_s": round(cam_px / (ms_step * 1e-3) / 1e6, 2),
+                "lidar_Mrays_s": round(lid_rays / (ms_step * 1e-3) / 1e6, 2),
+                "e2e": e2e, "gpu_launches": int(n_launch), "gpu_launches_per_step": int(n_launch // args.steps),
                 "host_enqueue_ms_per_step": round(host_enqueue_ms, 3),
-                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "stages": stage,
-                "per_config": per_config, "setup_s": {"generate": round(t_gen, 1)}}
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "parity": par, "stages": stage,
+                "per_config": per_config, "nccl": nccl, "setup_s": {"generate": round(t_gen, 1)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -554,6 +606,8 @@ def main():
                     help="N > 1: gather all frames after the batch (end) or one timestep round at a time as "
                          "soon as it is rendered, overlapping the transfer with rendering (rounds)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="enqueue every step eagerly instead of replaying a CUDA graph of the batch")
     ap.add_argument("--ref-rays", type=int, default=256)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -7,7 +7,7 @@
  * Conventions for every entry point
  *   - Ownership: the caller owns every buffer.  The library never allocates
  *     and holds no pointer after a call returns; its only process state is a
- *     relaxed kernel-launch counter and a cache of per-kernel occupancies.
+ *     relaxed kernel-launch counter.
  *   - Memory: pointers named d_* and all array pointers inside gs_surfels and
  *     the output/work buffers are DEVICE pointers (cudaMalloc / torch);
  *     gs_sensor.beam_elevation is a HOST pointer (copied into kernel
@@ -17,13 +17,19 @@
  *   - Errors: arguments are validated synchronously on the host before any
  *     launch: GS_ERR_CONFIG (null required pointer, wrong sensor kind for the
  *     call, sh_degree outside 0..3, width/height < 1, buffer too small),
- *     GS_ERR_RANGE (focal <= 0, non-monotone beam table, azimuth span outside
- *     (0, 2pi], theta_max outside (0, pi), tile shape outside 32..512
- *     samples or not a multiple of a 32-sample warp sub-tile), GS_ERR_CUDA
+ *     GS_ERR_RANGE (focal <= 0, non-finite principal point, camera wider or
+ *     taller than 65535 px, LiDAR wider than 32767 columns or with more than
+ *     GS_MAX_BEAMS beams, non-monotone beam table, non-finite azimuth0,
+ *     azimuth span outside (0, 2pi], theta_max outside (0, pi), a fisheye
+ *     lens theta_d(theta) not strictly increasing on [0, theta_max] (checked
+ *     on a 10^4-point grid, DESIGN reading R12), compositing constants out of
+ *     range, tile shape outside 32..512 samples or not a multiple of a
+ *     32-sample warp sub-tile), GS_ERR_CUDA
  *     (launch failure, from cudaGetLastError).  On any
  *     error nothing is enqueued after the failing launch; gs_last_error()
- *     returns a thread-local message.  Non-finite surfel inputs are not an
- *     error: such surfels are culled.
+ *     returns a thread-local message.  Surfels with a non-finite mean, scale
+ *     or depth, a scale <= 0 or an opacity <= 0 are not an error: they are
+ *     culled (they meet no ray).
  *   - Reentrancy: calls are pure functions of their inputs; concurrent calls
  *     on different streams with distinct output buffers are safe.
  *   - Determinism: no floating-point atomics; outputs are bitwise
@@ -156,7 +162,10 @@ gs_status gs_project(const gs_surfels *surfels, const gs_sensor *sensor, const g
                      gs_stream stream);
 
 /*
- * gs_bin_sort -- tile binning: a stable LSD radix sort of the 64-bit
+ * gs_bin_sort -- tile binning (the tile-based splatting of PAPER.md:48, whose
+ * per-tile depth-sorted lists the compositing walks front to back; sort order
+ * = the depth key of DESIGN reading R9, ties by surfel index): a stable LSD
+ * radix sort of the 64-bit
  * (tile << 32 | depth-key bits) pair keys (ties by surfel index), then tile
  * ranges.  The 32 depth bits are sorted once per visible surfel before the
  * pairs are emitted (an LSD sort may do its low digits on any order-preserving
@@ -184,7 +193,10 @@ gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sensor *sensor,
  * d_overflow (may be NULL) is gs_bin_sort's flag: if set, outputs are background.
  * workspace: device scratch of >= gs_render_workspace_bytes(pair_capacity, ...)
  * bytes (the pair_capacity given to gs_bin_sort): the longest-first tile
- * schedule and the partial composites of split tile lists.
+ * schedule and the partial composites of split tile lists.  The pair
+ * capacity is taken to be the largest one whose workspace fits in
+ * workspace_bytes; if the frame's pair count exceeds it (checked on the
+ * device) the outputs are background, as for d_overflow.
  * stats (may be NULL): device [2,H,W] u32 diagnostic counts per sample --
  * surfels composited, (sample, surfel) pairs whose conservative pixel box
  * contains the sample.  Non-NULL selects an instrumented kernel.
@@ -214,6 +226,71 @@ gs_status gs_render_lidar(const void *projected, int64_t n, const uint32_t *valu
                           const gs_sensor *sensor, const gs_opts *opts, void *workspace,
                           size_t workspace_bytes, float *range, float *intensity,
                           float *raydrop, float *alpha, uint32_t *stats, gs_stream stream);
+
+/* ------------------------------------------------------------------------
+ * Neural-Gaussian decode, the step upstream of
+ * gs_project: PAPER.md:78 (§III-A "Scene Reconstruction") -- the final 2DGS
+ * attributes {mu, R, S, rho, r, alpha} of each neural Gaussian are inferred
+ * by passing the anchor features through per-head MLPs (Scaffold-GS anchors,
+ * PAPER.md:49).  The paper fixes no sizes; DESIGN.md §12 readings N1-N6:
+ * GS_NEURAL_K surfels per anchor, GS_NEURAL_F features, per head two hidden
+ * layers of GS_NEURAL_HIDDEN with ReLU; geometry heads (offset, scale,
+ * rotation) read the feature, appearance heads read [feature, d] with
+ * d = normalize(position - view_origin).
+ */
+#define GS_NEURAL_K 5
+#define GS_NEURAL_F 32
+#define GS_NEURAL_HIDDEN 32
+
+typedef enum { GS_DECODE_CAMERA = 0, GS_DECODE_LIDAR = 1 } gs_decode_modality;
+
+/* heads, in this order (head index = position):
+ *   camera: OFFSET (15 = 3k), SCALE (10), ROTATION (30, 6D per surfel), OPACITY (5), COLOR (15)
+ *   LiDAR : OFFSET, SCALE, ROTATION, OPACITY, INTENSITY (5), RAYDROP (5)           */
+enum { GS_HEAD_OFFSET = 0, GS_HEAD_SCALE = 1, GS_HEAD_ROTATION = 2, GS_HEAD_OPACITY = 3,
+       GS_HEAD_COLOR = 4, GS_HEAD_INTENSITY = 4, GS_HEAD_RAYDROP = 5 };
+
+typedef struct {                 /* device pointers, read-only */
+    int64_t n;                   /* anchors, >= 0                                       */
+    const float *position;       /* [n,3] world metres                                  */
+    const uint16_t *feature;     /* [n,GS_NEURAL_F] IEEE fp16 bits, 16-byte aligned     */
+    const float *base_scale;     /* [n,3] > 0                                           */
+} gs_anchors;
+
+typedef struct {                 /* one MLP: device pointers, read-only                 */
+    const uint16_t *w1;          /* [HIDDEN, in] fp16 row-major; in = F (geometry heads)
+                                    or F+3 (appearance heads: feature then d)           */
+    const float *b1;             /* [HIDDEN]                                            */
+    const uint16_t *w2;          /* [HIDDEN, HIDDEN] fp16                               */
+    const float *b2;             /* [HIDDEN]                                            */
+    const uint16_t *w3;          /* [out, HIDDEN] fp16 (out per head, see above)        */
+    const float *b3;             /* [out]                                               */
+} gs_mlp;
+
+typedef struct {
+    int32_t modality;            /* gs_decode_modality                                  */
+    gs_mlp head[6];              /* 5 (camera) or 6 (LiDAR) heads                       */
+} gs_decoder;
+
+/*
+ * gs_decode_anchors -- anchors -> the 5n surfels of a gs_surfels set, surfel 5a+j
+ * from anchor a, output slot j, written to caller-owned device arrays:
+ *   means [5n,3]   = position + offset_j * base_scale (elementwise)
+ *   quats [5n,4]   (w,x,y,z), w >= 0, of the Gram-Schmidt frame (t_u, t_v,
+ *                  t_u x t_v) of the 6D rotation output (a1, a2)
+ *   scales [5n,2]  = (base_scale_0 exp(S_j0), base_scale_1 exp(S_j1))
+ *   opacities [5n] = sigmoid(.)
+ *   camera: sh [5n,1,3] = (sigmoid(colour) - 1/2) / C0 (degree-0 SH, so that
+ *           gs_project's colour is the decoded colour); intensity/raydrop unused
+ *   LiDAR : intensity [5n] = sigmoid(.), raydrop_logit [5n] = raw output; sh unused
+ * Arithmetic: fp16 tensor-core MMAs (tcgen05) with fp32 accumulation; hidden
+ * activations and d are rounded to fp16 (parity tolerance: DESIGN.md §12).
+ * Errors: GS_ERR_CONFIG for a NULL required pointer, an unknown modality,
+ * n < 0 or a feature pointer not 16-byte aligned.  n = 0 launches nothing.
+ */
+gs_status gs_decode_anchors(const gs_anchors *anchors, const gs_decoder *decoder, const float view_origin[3],
+                            float *means, float *quats, float *scales, float *opacities, float *sh,
+                            float *intensity, float *raydrop_logit, gs_stream stream);
 
 const char *gs_status_string(gs_status status);
 const char *gs_last_error(void);

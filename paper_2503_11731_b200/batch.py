@@ -148,11 +148,66 @@ class BatchRenderer:
                 times.render.append(ev[2].elapsed_time(ev[3]))
         return outs
 
+    def capture(self, sensors, outs, on_frame=None, join=()) -> "torch.cuda.CUDAGraph":
+        """Capture render(sensors, outs) -- every frame's gs_project ->
+        gs_bin_sort -> render launches on all lanes, with their cross-stream
+        ordering -- as one CUDA graph (capacity mode has no host sync, so the
+        whole batch is capturable).  Replaying it issues the batch with one
+        host call instead of ~20 library calls per frame.  The lanes' buffers
+        are sized by an eager render first, so nothing is allocated inside the
+        capture.  Call plan() first; the graph keeps pointing at `outs` and at
+        the surfel set current at capture time.  `join`: other streams
+        on_frame enqueues work on (e.g. a copy stream), joined back into the
+        capture at its end."""
+        sensors = self.wrap(sensors)
+        self.render(sensors, outs)            # eager pass: buffers at their final sizes
+        torch.cuda.synchronize(self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self.render(sensors, outs, on_frame=on_frame)
+                for js in join:
+                    side.wait_stream(js)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        return g
+
     def set_surfels(self, surfels: dict):
-        """Render from another device copy of the same surfel set (same count and
-        layout; e.g. a double buffer that the next batch is uploaded into)."""
+        """Render from another device surfel set: another copy of the same set
+        (a double buffer the next batch is uploaded into) keeps the planned
+        capacities; a set of another size (a streamed active set) needs a new
+        plan() (or render_checked)."""
+        if int(surfels["means"].shape[0]) != self.n:
+            self.caps = None
         for lane in self.lanes:
             lane.set_surfels(surfels)
+        self.n = self.lanes[0].n
+
+    def render_checked(self, sensors, outs, headroom: float = 1.25):
+        """Render with the planned capacities, then re-render every frame
+        whose pair count exceeded its capacity with a capacity grown to
+        `headroom` x its exact count (one sync).  The capacity policy of a
+        simulator whose poses are not known in advance: plan once, over-
+        provision, and repair the rare overflow.  Returns the re-rendered
+        frame indices."""
+        sensors = self.wrap(sensors)
+        if self.caps is None or len(self.caps) != len(sensors):
+            self.plan(sensors)
+        self.render(sensors, outs)
+        torch.cuda.synchronize(self.device)
+        bad = self.overflowed()
+        lane = self.lanes[0]
+        for i in bad:
+            _, d_np = lane.project(sensors[i], opts=self.frame_opts[i])
+            self.caps[i] = int(int(d_np.item()) * headroom) + 1
+            self.ovf[i:i + 1].zero_()
+            lane.render(sensors[i], out=outs[i], capacity=self.caps[i], overflow=self.ovf[i:i + 1],
+                        opts=self.frame_opts[i])
+        torch.cuda.synchronize(self.device)
+        assert not self.overflowed()
+        return bad
 
     def opts_of(self, i: int):
         """Options frame i of the planned batch is rendered with (None: the lane's default)."""

@@ -17,6 +17,8 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
                             int32_t *d_overflow, cudaStream_t st);
 size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix);
+cudaError_t launch_decode(const gs_anchors *, const gs_decoder *, const float[3], float *, float *, float *,
+                          float *, float *, float *, float *, cudaStream_t);
 cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
                                  const int32_t *, const DevSensor &, const DevOpts &, int32_t, void *,
                                  size_t, float *, float *, float *, float *, uint32_t *, cudaStream_t);
@@ -92,17 +94,40 @@ static gs_status check_sensor(const gs_sensor *s) {
     if (!s) return fail(GS_ERR_CONFIG, "sensor is NULL");
     if (s->kind < 0 || s->kind > 2) return fail(GS_ERR_CONFIG, "unknown sensor kind");
     if (s->width < 1 || s->height < 1) return fail(GS_ERR_CONFIG, "width/height < 1");
-    if (s->width > 32767 * 8 || s->height > 32767 * 8) return fail(GS_ERR_RANGE, "image too large");
+    // pixel boxes are packed as two u16 pairs (0xffff = empty); LiDAR column
+    // bounds run to 2W-1 across the azimuth seam
+    if (s->kind != GS_LIDAR_SPINNING && (s->width > 65535 || s->height > 65535))
+        return fail(GS_ERR_RANGE, "camera image wider or taller than 65535 px");
+    if (s->kind == GS_LIDAR_SPINNING && s->width > 32767)
+        return fail(GS_ERR_RANGE, "LiDAR wider than 32767 columns");
     if (s->kind != GS_LIDAR_SPINNING) {
         if (!(s->fx > 0.f) || !(s->fy > 0.f)) return fail(GS_ERR_RANGE, "focal length must be > 0");
-        if (s->kind == GS_FISHEYE_EQUIDISTANT && !(s->theta_max > 0.f && s->theta_max < (float)M_PI))
-            return fail(GS_ERR_RANGE, "theta_max outside (0, pi)");
+        if (!std::isfinite(s->cx) || !std::isfinite(s->cy)) return fail(GS_ERR_RANGE, "principal point not finite");
+        if (s->kind == GS_FISHEYE_EQUIDISTANT) {
+            if (!(s->theta_max > 0.f && s->theta_max < (float)M_PI))
+                return fail(GS_ERR_RANGE, "theta_max outside (0, pi)");
+            // the KB lens must be invertible on [0, theta_max] (DESIGN reading R12):
+            // theta_d' = 1 + 3k1 t^2 + 5k2 t^4 + 7k3 t^6 + 9k4 t^8 > 0 on a 10^4-point
+            // grid and theta_d(theta_max) > 0
+            const double k1 = s->k[0], k2 = s->k[1], k3 = s->k[2], k4 = s->k[3];
+            if (!std::isfinite(k1 + k2 + k3 + k4)) return fail(GS_ERR_RANGE, "fisheye k not finite");
+            const double tm = s->theta_max;
+            for (int i = 0; i <= 10000; ++i) {
+                const double t = tm * i / 10000.0, t2 = t * t;
+                const double dd = 1.0 + t2 * (3.0 * k1 + t2 * (5.0 * k2 + t2 * (7.0 * k3 + t2 * 9.0 * k4)));
+                if (!(dd > 0.0)) return fail(GS_ERR_RANGE, "fisheye lens not monotone on [0, theta_max]");
+            }
+            const double t2 = tm * tm;
+            if (!(tm * (1.0 + t2 * (k1 + t2 * (k2 + t2 * (k3 + t2 * k4)))) > 0.0))
+                return fail(GS_ERR_RANGE, "fisheye theta_d(theta_max) <= 0");
+        }
     } else {
         if (!s->beam_elevation) return fail(GS_ERR_CONFIG, "beam_elevation is NULL");
         if (s->height > GS_MAX_BEAMS) return fail(GS_ERR_RANGE, "more than GS_MAX_BEAMS beams");
         for (int r = 1; r < s->height; ++r)
             if (!(s->beam_elevation[r] < s->beam_elevation[r - 1]))
                 return fail(GS_ERR_RANGE, "beam elevations must be strictly decreasing");
+        if (!std::isfinite(s->azimuth0)) return fail(GS_ERR_RANGE, "azimuth0 not finite");
         const double span = (double)s->width * (double)s->azimuth_step;
         if (!(s->azimuth_step > 0.f) || !(span <= 2.0 * M_PI * (1.0 + 1e-6)))
             return fail(GS_ERR_RANGE, "azimuth span outside (0, 2pi]");
@@ -308,6 +333,34 @@ extern "C" gs_status gs_render_lidar(const void *projected, int64_t n, const uin
                                         workspace, workspace_bytes, range, intensity, raydrop, alpha, stats,
                                         (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_render_lidar");
+    return GS_OK;
+}
+
+extern "C" gs_status gs_decode_anchors(const gs_anchors *an, const gs_decoder *de, const float view_origin[3],
+                                       float *means, float *quats, float *scales, float *opacities, float *sh,
+                                       float *intensity, float *raydrop_logit, gs_stream stream) {
+    if (!an || !de || !view_origin) return fail(GS_ERR_CONFIG, "anchors, decoder or view_origin is NULL");
+    if (an->n < 0) return fail(GS_ERR_CONFIG, "anchor count < 0");
+    if (de->modality != GS_DECODE_CAMERA && de->modality != GS_DECODE_LIDAR)
+        return fail(GS_ERR_CONFIG, "unknown decode modality");
+    if (!(std::isfinite(view_origin[0]) && std::isfinite(view_origin[1]) && std::isfinite(view_origin[2])))
+        return fail(GS_ERR_RANGE, "view_origin not finite");
+    if (an->n == 0) return GS_OK;
+    if (!an->position || !an->feature || !an->base_scale) return fail(GS_ERR_CONFIG, "anchor array is NULL");
+    if (((uintptr_t)an->feature & 15u) != 0) return fail(GS_ERR_CONFIG, "feature pointer not 16-byte aligned");
+    const int H = de->modality == GS_DECODE_LIDAR ? 6 : 5;
+    for (int h = 0; h < H; ++h) {
+        const gs_mlp &m = de->head[h];
+        if (!m.w1 || !m.b1 || !m.w2 || !m.b2 || !m.w3 || !m.b3) return fail(GS_ERR_CONFIG, "decoder weight is NULL");
+    }
+    if (!means || !quats || !scales || !opacities) return fail(GS_ERR_CONFIG, "output array is NULL");
+    if (de->modality == GS_DECODE_CAMERA && !sh) return fail(GS_ERR_CONFIG, "camera decode needs sh");
+    if (de->modality == GS_DECODE_LIDAR && (!intensity || !raydrop_logit))
+        return fail(GS_ERR_CONFIG, "LiDAR decode needs intensity and raydrop_logit");
+    if (((uintptr_t)quats & 15u) != 0) return fail(GS_ERR_CONFIG, "quats pointer not 16-byte aligned");
+    const cudaError_t e = launch_decode(an, de, view_origin, means, quats, scales, opacities, sh, intensity,
+                                        raydrop_logit, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_decode_anchors");
     return GS_OK;
 }
 

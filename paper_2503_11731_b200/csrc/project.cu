@@ -360,8 +360,8 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
 // its centre fails the depth-key test (exact, the same pinned key as
 // k_project) or when the sphere of radius 3.001 max(s_u, s_v) around its
 // sensor-frame centre (which holds the 3-sigma support disk) lies outside
-// the sensor's field of view widened by a margin (pinhole: 4 px beyond the
-// image, covering the low-pass disc; fisheye: 0.15 rad beyond theta_max), or
+// the sensor's field of view widened by a margin (pinhole: the low-pass disc
+// radius + 1 px beyond the image; fisheye: 0.15 rad beyond theta_max), or
 // (LiDAR) when no beam's elevation lies in the elevation range of the support
 // disk, bounded from its exact z-extent and horizontal distance range (+1e-4
 // in sine).  fp32 arithmetic with margins well above its error; a culled
@@ -394,7 +394,8 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
                     1e-3f * (1.f + fabsf(X) + fabsf(Y) + fabsf(Z));
     if (!isfinite(X + Y + Z + R)) return true;   // let k_project decide
     if (KIND == GS_PINHOLE) {
-        const float m = 4.f;
+        // margin: the low-pass disc radius sqrt(rcut) sigma (the same cut as k_project) + 1 px
+        const float m = 1.f + sqrtf(op.support * 1.0001f + 1e-4f) * sqrtf(op.sigma2);
         const float xl = (-m - se.cx) / se.fx, xr = ((float)se.width + m - se.cx) / se.fx;
         const float yl = (-m - se.cy) / se.fy, yr = ((float)se.height + m - se.cy) / se.fy;
         if ((X - xl * Z) < -R * sqrtf(1.f + xl * xl)) return false;
@@ -648,8 +649,12 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                     if (!allaz) {
                         // column bounds widened by one column below: a reciprocal step is exact enough
                         const double step = (double)se.az_step, istep = 1.0 / step;
-                        const double ulo = (ab.azc + ab.daz_lo - (double)se.az0) * istep;
-                        const double uhi = (ab.azc + ab.daz_hi - (double)se.az0) * istep;
+                        // start of the azimuth interval relative to az0, reduced into [0, 2pi)
+                        // (az0 may be any angle; the interval is at most one turn wide)
+                        double a0 = fmod(ab.azc + ab.daz_lo - (double)se.az0, 2.0 * M_PI);
+                        if (a0 < 0.0) a0 += 2.0 * M_PI;
+                        const double ulo = a0 * istep;
+                        const double uhi = (a0 + (ab.daz_hi - ab.daz_lo)) * istep;
                         double jlo = ceil(ulo) - 1.0, jhi = floor(uhi) + 1.0;
                         if (se.full_turn) {
                             if (jhi - jlo + 1.0 >= (double)W) {
@@ -665,10 +670,11 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                                 c1 = (int)jhi;   // may exceed W-1: wraps
                             }
                         } else {
-                            // partial turn: union of the shifts by +-2pi, hull
+                            // partial turn: the interval starts in [0, 2pi) past az0, so only
+                            // it and its shift by -2pi can meet the columns [0, W); hull
                             const double per = 2.0 * M_PI / step;
                             double lo = 1e30, hi = -1e30;
-                            for (int kk = -1; kk <= 1; ++kk) {
+                            for (int kk = -1; kk <= 0; ++kk) {
                                 const double a0 = fmax(jlo + kk * per, 0.0), a1 = fmin(jhi + kk * per, (double)(W - 1));
                                 if (a0 <= a1) { lo = fmin(lo, a0); hi = fmax(hi, a1); }
                             }
@@ -919,18 +925,15 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     // grid-stride k_project: exactly the resident CTAs (whole waves, no tail wave)
-    static int occ[3] = {0, 0, 0};
-    if (!occ[se.kind]) {
-        int o = 0;
-        if (se.kind == GS_PINHOLE)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_PINHOLE>, 256, 0);
-        else if (se.kind == GS_FISHEYE_EQUIDISTANT)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_FISHEYE_EQUIDISTANT>, 256, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_project<GS_LIDAR_SPINNING>, 256, 0);
-        occ[se.kind] = o > 0 ? o : 1;
-    }
-    const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * occ[se.kind]);
+    // (queried per call: the library keeps no mutable process state besides the launch counter)
+    int occ = 0;
+    if (se.kind == GS_PINHOLE)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_PINHOLE>, 256, 0);
+    else if (se.kind == GS_FISHEYE_EQUIDISTANT)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_FISHEYE_EQUIDISTANT>, 256, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_LIDAR_SPINNING>, 256, 0);
+    const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * std::max(occ, 1));
     note_launch(3);   // k_cull + k_project + k_compact
     if (se.kind == GS_PINHOLE) {
         k_cull<GS_PINHOLE><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);

@@ -76,7 +76,7 @@ struct SchedHdr {
     uint32_t rw_count;       // re-walk items (split tile, segment) appended by k_merge_plan
     uint32_t rw_counter;     // persistent work counter of k_rewalk
     uint32_t P;              // total pairs (max tile range end)
-    uint32_t pad0;
+    uint32_t ovf;            // P exceeds the capacity the workspace was sized for: render background
     uint32_t bucket_cnt[NB];
     uint32_t bucket_cur[NB];
     uint32_t pad1[24];
@@ -701,11 +701,20 @@ __device__ __forceinline__ uint32_t seg_len(const SchedHdr *h, uint32_t lfix, ui
 }
 
 // ---------------------------------------------------------------- schedule
-__global__ void k_sched_total(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow, SchedHdr *h) {
+// d_overflow (gs_bin_sort's flag) or a pair count above the capacity the
+// render workspace was sized for: the frame renders as background (nothing
+// below reads past the workspace)
+__device__ __forceinline__ bool frame_ovf(const int32_t *d_overflow, const SchedHdr *h) {
+    return (d_overflow && *d_overflow) || h->ovf;
+}
+
+__global__ void k_sched_total(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow, SchedHdr *h,
+                              uint64_t cap) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles || (d_overflow && *d_overflow)) return;
     const uint32_t e = ranges[t].y;
     if (e) atomicMax(&h->P, e);
+    if (e > cap) h->ovf = 1u;
 }
 
 __global__ void k_sched_count(const uint2 *__restrict__ ranges, int ntiles, const int32_t *d_overflow,
@@ -713,7 +722,7 @@ __global__ void k_sched_count(const uint2 *__restrict__ ranges, int ntiles, cons
     const uint32_t L = seg_len(h, lfix, ctas);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
-    const bool ovf = d_overflow && *d_overflow;
+    const bool ovf = frame_ovf(d_overflow, h);
     const uint2 rg = ranges[t];
     const uint32_t len = ovf ? 0u : rg.y - rg.x;
     atomicAdd(&h->bucket_cnt[bucket_of(len, L)], seg_count(len, L));
@@ -738,7 +747,7 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
     const uint32_t L = seg_len(h, lfix, ctas);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
-    const bool ovf = d_overflow && *d_overflow;
+    const bool ovf = frame_ovf(d_overflow, h);
     const uint2 rg = ranges[t];
     const uint32_t len = ovf ? 0u : rg.y - rg.x;
     const uint32_t ns = seg_count(len, L);
@@ -771,7 +780,7 @@ __device__ __forceinline__ void render_body(
     const bool piped = blockDim.x > 32;   // one-warp tiles stage for themselves
     const int nw = piped ? (int)(blockDim.x >> 5) - 1 : 1, npix = nw * 32;
     const bool cons = warp < nw;
-    const bool ovf = d_overflow && *d_overflow;
+    const bool ovf = frame_ovf(d_overflow, h);
     const uint32_t n_items = h->n_items;
     if (piped) pipe_init(pp, nw);
     uint32_t g = 0;
@@ -1028,7 +1037,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)W.max_items));
     const unsigned gt = (unsigned)((ntiles + 255) / 256);
     note_launch(4);
-    k_sched_total<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h);
+    k_sched_total<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, (uint64_t)cap);
     k_sched_count<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, lfix, ctas);
     k_sched_scan<<<1, 32, 0, st>>>(h);
     k_sched_fill<<<gt, 256, 0, st>>>((const uint2 *)ranges, ntiles, d_overflow, h, items, split_base, split_list,

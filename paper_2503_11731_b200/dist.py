@@ -41,8 +41,39 @@ def init(backend: str | None = None):
         kw = dict(backend=be, rank=rank, world_size=world)
         if be == "nccl":
             kw["device_id"] = device
+            # communicator set-up lines (INIT subsystem only) to a per-process file, echoed
+            # by nccl_init_info() so a run shows how many ranks the communicator joined
+            if "NCCL_DEBUG" not in os.environ:
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+                os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(
+                    os.environ.get("TMPDIR", "/tmp"), "gsr_nccl.%h.%p.log"))
         dist.init_process_group(**kw)
     return rank, world, device
+
+
+def nccl_init_info(echo: bool = True):
+    """This process's NCCL communicator set-up lines (NCCL_DEBUG_SUBSYS=INIT,
+    written to NCCL_DEBUG_FILE by init()); echoed to stderr.  Returns
+    {"nranks": [...], "init_complete": n, "lines": [...]} or None."""
+    import glob
+    import re
+    import socket
+    import sys
+    pat = os.environ.get("NCCL_DEBUG_FILE")
+    if not pat:
+        return None
+    path = pat.replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    files = [path] if os.path.exists(path) else glob.glob(pat.replace("%h", "*").replace("%p", str(os.getpid())))
+    lines = []
+    for f in files:
+        with open(f, errors="replace") as fh:
+            lines += [ln.rstrip() for ln in fh if "Init COMPLETE" in ln or "nranks" in ln or "NCCL version" in ln]
+    if echo:
+        for ln in lines[:16]:
+            print("[nccl]", ln, file=sys.stderr)
+    nr = sorted({int(m) for ln in lines for m in re.findall(r"nranks (\d+)", ln)})
+    return {"nranks": nr, "init_complete": sum("Init COMPLETE" in ln for ln in lines), "lines": lines[:8]}
 
 
 def shard_range(n_items: int, world: int, rank: int):
@@ -134,3 +165,68 @@ def round_ops(local: dict, full: dict | None, j: int, n_items: int, world: int, 
 
 def n_rounds(n_items: int, world: int) -> int:
     return max(shard_counts(n_items, world)) if world > 0 else 0
+
+
+class ShardedBatch:
+    """Output layout and gather of a frame-sharded batch (the bookkeeping of
+    bench.py's multi-GPU step).  The batch is n_t timesteps with the same
+    frames each (`frame_specs`: (kind, C, H, W) per frame of a timestep);
+    this rank renders timesteps [lo, hi) (shard_range).  Frames are stored in
+    one slab per kind in batch order: rank 0 allocates the whole batch
+    (`full`) and renders straight into its own slice, the other ranks hold
+    only their block (`local`).  `outs[i]` is the tensor local frame i (in
+    timestep-major order) is rendered into.  The only exchange is the gather
+    to rank 0: all at the end (`gather`) or one timestep round at a time
+    (`round`), overlapping the rendering of the next timesteps."""
+
+    def __init__(self, frame_specs, n_t: int, world: int, rank: int, device, dtype=torch.float32):
+        self.specs = list(frame_specs)
+        self.n_t, self.world, self.rank = n_t, world, rank
+        self.lo, self.hi = shard_range(n_t, world, rank)
+        self.kinds = sorted({int(k) for k, *_ in self.specs})
+        self.per_t = {k: sum(1 for s in self.specs if int(s[0]) == k) for k in self.kinds}
+        self.full, self.local = {}, {}
+        nloc = self.hi - self.lo
+        for k in self.kinds:
+            _, C, H, W = next(s for s in self.specs if int(s[0]) == k)
+            if rank == 0:
+                self.full[k] = torch.empty((n_t * self.per_t[k], C, H, W), dtype=dtype, device=device)
+                self.local[k] = self.full[k][self.per_t[k] * self.lo: self.per_t[k] * self.hi]
+            else:
+                self.local[k] = torch.empty((nloc * self.per_t[k], C, H, W), dtype=dtype, device=device)
+        self.outs = []
+        for j in range(nloc):
+            seen = {k: 0 for k in self.kinds}
+            for kind, *_ in self.specs:
+                k = int(kind)
+                self.outs.append(self.local[k][j * self.per_t[k] + seen[k]])
+                seen[k] += 1
+        self.local_blocks = {k: self.local[k].view(nloc, self.per_t[k], *self.local[k].shape[1:])
+                             for k in self.kinds}
+        self.full_blocks = ({k: self.full[k].view(n_t, self.per_t[k], *self.full[k].shape[1:])
+                             for k in self.kinds} if rank == 0 else None)
+
+    @property
+    def frames_per_timestep(self) -> int:
+        return len(self.specs)
+
+    def gather(self):
+        """Gather every rank's block to rank 0 (point-to-point), and wait."""
+        if self.world == 1:
+            return
+        reqs = []
+        for k in self.kinds:
+            fv = self.full_blocks[k] if self.full_blocks is not None else None
+            reqs += gather_blocks(self.local_blocks[k], fv, self.n_t, self.world, self.rank)
+        for r in reqs:
+            r.wait()
+
+    def round(self, j: int):
+        """Post gather round j (item j of every rank's block); returns the requests."""
+        ops = round_ops(self.local_blocks, self.full_blocks, j, self.n_t, self.world, self.rank)
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def rounds_left(self):
+        """Rounds rank 0 still has to receive after posting one per own timestep
+        (uneven blocks: peers with more timesteps than the root)."""
+        return range(self.hi - self.lo, n_rounds(self.n_t, self.world)) if self.rank == 0 else range(0)

@@ -51,7 +51,25 @@ class gs_opts(C.Structure):
                 ("grid_share", C.c_float)]
 
 
-EXPORTS = ["gs_default_opts", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
+GS_DECODE_CAMERA, GS_DECODE_LIDAR = 0, 1
+GS_NEURAL_K, GS_NEURAL_F, GS_NEURAL_HIDDEN = 5, 32, 32
+
+
+class gs_anchors(C.Structure):
+    _fields_ = [("n", C.c_int64), ("position", C.c_void_p), ("feature", C.c_void_p),
+                ("base_scale", C.c_void_p)]
+
+
+class gs_mlp(C.Structure):
+    _fields_ = [("w1", C.c_void_p), ("b1", C.c_void_p), ("w2", C.c_void_p), ("b2", C.c_void_p),
+                ("w3", C.c_void_p), ("b3", C.c_void_p)]
+
+
+class gs_decoder(C.Structure):
+    _fields_ = [("modality", C.c_int32), ("head", gs_mlp * 6)]
+
+
+EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
            "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes",
            "gs_kernel_launches"]
@@ -102,6 +120,8 @@ def load(build_if_missing: bool = True):
     lib.gs_status_string.restype = C.c_char_p
     lib.gs_last_error.argtypes = []
     lib.gs_last_error.restype = C.c_char_p
+    lib.gs_decode_anchors.argtypes = [P(gs_anchors), P(gs_decoder), vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.gs_decode_anchors.restype = C.c_int
     lib.gs_kernel_launches.argtypes = []
     lib.gs_kernel_launches.restype = C.c_uint64
     _lib = lib
@@ -225,6 +245,14 @@ def gs_render_lidar(projected, n, values, tile_ranges, d_overflow, sensor: Senso
                                   workspace.numel() * workspace.element_size(), _ptr(rng),
                                   _ptr(intensity), _ptr(raydrop), _ptr(alpha), _ptr(stats),
                                   C.c_void_p(stream)))
+
+
+def gs_decode_anchors(anchors: gs_anchors, decoder: gs_decoder, view_origin, means, quats, scales, opacities,
+                      sh, intensity, raydrop_logit, stream):
+    origin = (C.c_float * 3)(*[float(v) for v in view_origin])
+    _check(load().gs_decode_anchors(C.byref(anchors), C.byref(decoder), origin, _ptr(means), _ptr(quats),
+                                    _ptr(scales), _ptr(opacities), _ptr(sh), _ptr(intensity),
+                                    _ptr(raydrop_logit), C.c_void_p(stream)))
 
 
 def gs_kernel_launches() -> int:

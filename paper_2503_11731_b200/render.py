@@ -52,9 +52,11 @@ class Renderer:
         self.last_pairs = None
 
     def set_surfels(self, surfels: dict):
-        """Point the renderer at another device copy of a surfel set of the same size."""
-        assert int(surfels["means"].shape[0]) == self.n
+        """Point the renderer at another device surfel set (e.g. the other
+        half of a double buffer, or a streamed active set of another size;
+        the work buffers grow on demand)."""
         self.t = surfels
+        self.n = int(surfels["means"].shape[0])
         self.struct = gsr.surfels_struct(surfels)
 
     # buffers are cached per (name) and grown on demand

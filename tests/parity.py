@@ -13,8 +13,12 @@ alpha, normal, intensity, ray-drop; 1e-4 relative on depth and range):
     lie, channel by channel, inside the envelope of the variants widened by
     the same tolerances.
 
-Flagged rays may number at most MAX_FLAGGED_FRAC of the rays (the pre-kernel
-bound), and unresolved rays (more variants than the oracle enumerates) none.
+A flagged ray is "ambiguous" when its admissible results differ from each
+other by more than the tolerance (most flagged rays are not: e.g. a stop
+decision at T ~ 1e-4 changes the result by less than T).  Ambiguous rays may
+number at most MAX_AMBIGUOUS_FRAC of the rays (the pre-kernel flagged-ray
+bound, 2e-3); unresolved rays (more variants than the oracle enumerates)
+none.
 """
 from __future__ import annotations
 
@@ -24,7 +28,7 @@ import oracle
 
 TOL_ABS = 1e-4        # colour, alpha, normal, intensity, raydrop (north_star)
 TOL_REL = 1e-4        # depth, range (north_star)
-MAX_FLAGGED_FRAC = 2e-3
+MAX_AMBIGUOUS_FRAC = 2e-3
 MAX_VARIANTS = 256
 
 
@@ -90,6 +94,7 @@ def compare(gpu_chw: np.ndarray, ref: np.ndarray, flags: np.ndarray, rays: np.nd
     fidx = np.nonzero(fl)[0]
     bad_flagged = np.zeros(len(rays), bool)
     unresolved = 0
+    ambiguous = 0
     n_cond = 0
     nominal_ok = 0
     if len(fidx):
@@ -104,6 +109,9 @@ def compare(gpu_chw: np.ndarray, ref: np.ndarray, flags: np.ndarray, rays: np.nd
                     bad_flagged[i] = True
                     continue
                 v = var[k, :nv, :C]
+                # ambiguous: the admissible results differ by more than the tolerance
+                sa, sr, sb = _errors(v, v[:1].repeat(nv, 0), cam)
+                ambiguous += bool(np.any((sa > TOL_ABS) | (sr > TOL_REL) | sb))
                 ea, er, eb = _errors(g[i][None, :], v, cam)
                 match = (ea <= TOL_ABS) & (er <= TOL_REL) & ~eb
                 nominal_ok += bool(match[0])
@@ -113,7 +121,8 @@ def compare(gpu_chw: np.ndarray, ref: np.ndarray, flags: np.ndarray, rays: np.nd
                 else:
                     bad_flagged[i] = not match.any()
     uf = ~fl
-    stats = dict(n=len(rays), flagged=int(fl.sum()), flagged_cond=n_cond, unresolved=unresolved,
+    stats = dict(n=len(rays), flagged=int(fl.sum()), ambiguous=ambiguous, flagged_cond=n_cond,
+                 unresolved=unresolved,
                  flagged_nominal_match=int(nominal_ok),
                  bad=int(bad.sum()), bad_flagged=int(bad_flagged.sum()),
                  max_abs_unflagged=float(err_abs[uf].max()) if uf.any() else 0.0,
@@ -130,7 +139,7 @@ def compare(gpu_chw: np.ndarray, ref: np.ndarray, flags: np.ndarray, rays: np.nd
                        mean=float(np.abs(g[uf, c] - r[uf, c]).mean()) if uf.any() else 0.0)
         for c in range(C)}
     stats["ok"] = (stats["bad"] == 0 and stats["bad_flagged"] == 0 and unresolved == 0 and
-                   stats["flagged"] <= max(2, MAX_FLAGGED_FRAC * len(rays)))
+                   stats["ambiguous"] <= max(2, MAX_AMBIGUOUS_FRAC * len(rays)))
     if stats["bad"] or stats["bad_flagged"]:
         i = np.nonzero(bad | bad_flagged)[0][:5]
         stats["worst"] = [dict(ray=int(rays[k]), x=int(rays[k] % W), y=int(rays[k] // W), flag=int(flags[k]),

@@ -107,3 +107,69 @@ def test_sizes(gsr):
     assert offs["total"] == gsr.gs_projected_bytes(1000, 0)
     assert offs["rec"] == 256 and offs["rect"] >= 256 + 96 * 1000
     assert gsr.gs_sort_workspace_bytes(1000, 10_000, cam, o) > 10_000 * 12
+
+
+def test_host_validation_round2(gsr):
+    """Checks added in round 2: a non-monotone or non-finite fisheye lens,
+    oversized images (u16 pixel boxes), a non-finite azimuth0 (GS_ERR_RANGE)."""
+    th = float(np.float32(np.deg2rad(95)))
+    good = sg.fisheye(64, 48, th, np.zeros(4, np.float32), 32, 24, sg.identity_pose())
+    assert _call_project(gsr, gsr.Sensor(good)) != gsr.GS_ERR_RANGE
+    bad = sg.fisheye(64, 48, th, np.array([-0.45, 0.08, 0.0, 0.0], np.float32), 32, 24, sg.identity_pose())
+    k = bad.k.astype(np.float64)
+    t = np.linspace(0, th, 10001)
+    td = t * (1 + k[0] * t ** 2 + k[1] * t ** 4 + k[2] * t ** 6 + k[3] * t ** 8)
+    assert not np.all(np.diff(td) > 0)            # indeed not monotone on [0, theta_max]
+    assert _call_project(gsr, gsr.Sensor(bad)) == gsr.GS_ERR_RANGE
+    assert b"monotone" in gsr.load().gs_last_error()
+    nan = sg.fisheye(64, 48, th, np.array([np.nan, 0, 0, 0], np.float32), 32, 24, sg.identity_pose())
+    assert _call_project(gsr, gsr.Sensor(nan)) == gsr.GS_ERR_RANGE
+    big = sg.pinhole(70000, 10, 100.0, 5, 5, sg.identity_pose())
+    assert _call_project(gsr, gsr.Sensor(big)) == gsr.GS_ERR_RANGE
+    wide = sg.lidar64(sg.lidar_pose([0, 0, 0]), height=8, width=40000)
+    assert _call_project(gsr, gsr.Sensor(wide)) == gsr.GS_ERR_RANGE
+    az = sg.lidar64(sg.lidar_pose([0, 0, 0]), height=8, width=64)
+    az.azimuth0 = float("nan")
+    assert _call_project(gsr, gsr.Sensor(az)) == gsr.GS_ERR_RANGE
+
+
+def test_decode_anchors_validation(gsr):
+    """gs_decode_anchors host checks: NULL structs, unknown modality, NULL
+    weights or outputs, misaligned features; n = 0 launches nothing."""
+    lib = gsr.load()
+    an = gsr.gs_anchors()
+    de = gsr.gs_decoder()
+    o3 = (C.c_float * 3)(0, 0, 0)
+    d = C.c_void_p(16)
+    assert lib.gs_decode_anchors(None, C.byref(de), o3, d, d, d, d, d, None, None, None) == gsr.GS_ERR_CONFIG
+    an.n = 0
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, None, None, None, None, None, None, None,
+                                 None) == gsr.GS_OK
+    de.modality = 7
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, d, d, d, d, d, None, None, None) == gsr.GS_ERR_CONFIG
+    de.modality = gsr.GS_DECODE_CAMERA
+    an.n, an.position, an.feature, an.base_scale = 10, 16, 16, 16
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, d, d, d, d, d, None, None, None) == gsr.GS_ERR_CONFIG
+    assert b"weight" in lib.gs_last_error()
+    for h in range(6):
+        m = de.head[h]
+        m.w1 = m.b1 = m.w2 = m.b2 = m.w3 = m.b3 = 16
+    an.feature = 18   # misaligned
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, d, d, d, d, d, None, None, None) == gsr.GS_ERR_CONFIG
+    an.feature = 16
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, d, d, d, d, None, None, None, None) == gsr.GS_ERR_CONFIG
+    de.modality = gsr.GS_DECODE_LIDAR
+    assert lib.gs_decode_anchors(C.byref(an), C.byref(de), o3, d, d, d, d, None, d, None, None) == gsr.GS_ERR_CONFIG
+
+
+def test_decode_kernel_uses_tcgen05():
+    """The decode kernel's SASS issues 5th-gen tensor-core MMAs (UTCHMMA) and
+    reads tensor memory (LDTM)."""
+    import subprocess
+    from paper_2503_11731_b200 import build
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.SO],
+                          capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    dec = [f for f in funcs if f.startswith("_ZN3gsr3dec8k_decode")]
+    assert len(dec) == 2   # camera and LiDAR instantiations
+    assert all("UTCHMMA" in f and "LDTM" in f for f in dec)

@@ -133,3 +133,67 @@ def test_overlapped_gather_rounds_gloo(world, n_t):
         p.join(timeout=60)
     assert res[0] == "ok" and res[1], res
     assert all(p.exitcode == 0 for p in ps)
+
+
+def _bench_worker(rank, world, port, n_t, schedule, q):
+    """bench.py's multi-GPU step bookkeeping (dist.ShardedBatch: slabs, the
+    per-frame output views, the timestep shard, both gather schedules) with a
+    stub renderer in place of the CUDA path: frame f of timestep t is filled
+    with a deterministic function of (t, f)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        # a timestep as in the Chunked batch: 6 cameras (8 channels) then 1 LiDAR (4)
+        specs = [(0, 8, 3, 5)] * 6 + [(2, 4, 2, 6)]
+        sb = gd.ShardedBatch(specs, n_t, world, rank, torch.device("cpu"))
+        lo, hi = gd.shard_range(n_t, world, rank)
+        assert (sb.lo, sb.hi) == (lo, hi) and len(sb.outs) == 7 * (hi - lo)
+        fpt = sb.frames_per_timestep
+
+        def stub(t, f):
+            return _frame(1000 * t + f, tuple(specs[f][1:]))
+        reqs = []
+        for i, out in enumerate(sb.outs):
+            t, f = lo + i // fpt, i % fpt
+            out.copy_(stub(t, f))                      # "render" local frame i
+            if schedule == "rounds" and f == fpt - 1:
+                reqs += sb.round(i // fpt)             # post this timestep's round
+        if schedule == "rounds":
+            for j in sb.rounds_left():
+                reqs += sb.round(j)
+            for r in reqs:
+                r.wait()
+        else:
+            sb.gather()
+        if rank == 0:
+            ok = True
+            for t in range(n_t):
+                cams = [f for f in range(7) if specs[f][0] == 0]
+                for c, f in enumerate(cams):
+                    ok &= torch.equal(sb.full[0][6 * t + c], stub(t, f))
+                ok &= torch.equal(sb.full[2][t], stub(t, 6))
+            q.put(("ok", bool(ok), None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), None))
+
+
+@pytest.mark.parametrize("schedule", ["end", "rounds"])
+@pytest.mark.parametrize("world,n_t", [(4, 10), (4, 3)])
+def test_bench_step_bookkeeping_world4_gloo(world, n_t, schedule):
+    """World size 4: the sharding, slab and gather bookkeeping bench.py's step
+    runs (both gather schedules, uneven and short blocks) assembles the whole
+    batch on rank 0 in batch order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_bench_worker, args=(r, world, port, n_t, schedule, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=180)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == "ok" and res[1], res
+    assert all(p.exitcode == 0 for p in ps)

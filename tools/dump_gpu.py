@@ -4,6 +4,9 @@ against the oracle on the dev box (the oracle is not run here).
 
 python tools/dump_gpu.py OUTDIR [which ...]
 which: mid fisheye lidar chunked   (default: all)
+python tools/dump_gpu.py OUTDIR full CONFIG ROW0 ROW1
+    all pixels of rows [ROW0, ROW1) of the config's frame (full-frame parity
+    in slabs small enough for gpurun_out)
 """
 import os
 import sys
@@ -34,8 +37,17 @@ def save(outdir, name, img, rays):
 
 def main():
     outdir = sys.argv[1]
-    which = sys.argv[2:] or ["mid", "fisheye", "lidar", "chunked"]
     os.makedirs(outdir, exist_ok=True)
+    if len(sys.argv) > 2 and sys.argv[2] == "full":
+        name, r0, r1 = sys.argv[3], int(sys.argv[4]), int(sys.argv[5])
+        c = sg.make_config(name)
+        se = c.sensors[0]
+        img = Renderer(to_device(c.surfels)).render(se).cpu().numpy()
+        r1 = min(r1, se.height)
+        rays = np.arange(r0 * se.width, r1 * se.width, dtype=np.int64)
+        save(outdir, f"{name}_full_{r0}_{r1}", img, rays)
+        return
+    which = sys.argv[2:] or ["mid", "fisheye", "lidar", "chunked"]
     for name in which:
         if name == "chunked":
             s = sg.chunked_surfels()
