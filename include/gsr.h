@@ -70,7 +70,11 @@ typedef enum {
 typedef enum {
     GS_PINHOLE = 0,               /* PAPER.md:96-100, Eq. 3                        */
     GS_FISHEYE_EQUIDISTANT = 1,   /* BASELINE Fisheye config; replaces Eq. 4 (DESIGN R4) */
-    GS_LIDAR_SPINNING = 2         /* PAPER.md:108-114, Eq. 5                       */
+    GS_LIDAR_SPINNING = 2,        /* PAPER.md:108-114, Eq. 5                       */
+    GS_FISHEYE_CYLINDRICAL = 3    /* PAPER.md:102-106, Eq. 4 (cylindrical projection):
+                                     column -> azimuth phi = (p_x - c_x)/f_x about the
+                                     camera y axis, row -> p_y = c_y + f_y y / sqrt(x^2+z^2)
+                                     (DESIGN reading R20); rendered by gs_render_camera */
 } gs_sensor_kind;
 
 #define GS_MAX_BEAMS 256
@@ -96,7 +100,8 @@ typedef struct {
     int32_t kind;                /* gs_sensor_kind                                      */
     int32_t width, height;       /* pixels; LiDAR: width = azimuth columns, height = beams */
     float world_to_sensor[12];
-    float fx, fy, cx, cy;        /* cameras: pixel (i,j) samples (i+1/2, j+1/2)         */
+    float fx, fy, cx, cy;        /* cameras: pixel (i,j) samples (i+1/2, j+1/2);
+                                    cylindrical: the columns' azimuths must lie in [-pi, pi] */
     float k[4];                  /* fisheye Kannala-Brandt k1..k4 (theta_d polynomial)  */
     float theta_max;             /* fisheye half field of view (rad), in (0, pi)       */
     const float *beam_elevation; /* LiDAR [height] elevations (rad), strictly decreasing, HOST */

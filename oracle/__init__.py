@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "oracle.c")
 
-PINHOLE, FISHEYE, LIDAR = 0, 1, 2
+PINHOLE, FISHEYE, LIDAR, CYLINDRICAL = 0, 1, 2, 3
 F_ALPHA, F_SUPPORT, F_NEAR, F_TSTOP, F_FOV, F_BRANCH, F_COND = 1, 2, 4, 8, 16, 32, 64
 
 

@@ -79,6 +79,9 @@ def _ray(se, col, row):
         psi = np.arctan2(m[1], m[0]) if td > 0 else 0.0
         d = np.array([np.sin(th) * np.cos(psi), np.sin(th) * np.sin(psi), np.cos(th)])
         return d, p, td <= tdmax
+    if se.kind == 3:   # cylindrical (Eq. 4): azimuth about y, height over the y-axis distance
+        phi = (p[0] - se.cx) / se.fx
+        return np.array([np.sin(phi), (p[1] - se.cy) / se.fy, np.cos(phi)]), p, True
     th = float(se.beam_elevation[row])
     ph = float(se.azimuth0) + col * float(se.azimuth_step)
     return np.array([np.cos(th) * np.cos(ph), np.cos(th) * np.sin(ph), np.sin(th)]), p, True
@@ -114,6 +117,10 @@ def _prep(s, se, o):
         safe = np.where(rxy > 0, rxy, 1.0)
         c = np.stack([np.where(rxy > 0, se.cx + se.fx * td * mus[:, 0] / safe, se.cx),
                       np.where(rxy > 0, se.cy + se.fy * td * mus[:, 1] / safe, se.cy)], 1)
+        cdepth = np.linalg.norm(mus, axis=1)
+    elif se.kind == 3:
+        c = np.stack([se.cx + se.fx * np.arctan2(mus[:, 0], mus[:, 2]),
+                      se.cy + se.fy * mus[:, 1] / np.hypot(mus[:, 0], mus[:, 2])], 1)
         cdepth = np.linalg.norm(mus, axis=1)
     else:
         c = np.zeros((s.n, 2))

@@ -142,6 +142,12 @@ static void project_centre(const or_sensor *se, const double m[3], double c[2]) 
         } else {
             c[0] = se->cx; c[1] = se->cy;
         }
+    } else if (se->kind == OR_CYLINDRICAL) {
+        /* Eq. 4 (reading R20): azimuth about the camera y axis ->
+         * column, y over the distance from the y axis -> row */
+        const double rho = sqrt(m[0] * m[0] + m[2] * m[2]);
+        c[0] = (double)se->cx + (double)se->fx * atan2(m[0], m[2]);
+        c[1] = (double)se->cy + (double)se->fy * m[1] / rho;
     } else {
         c[0] = c[1] = 0.0;
     }
@@ -227,6 +233,21 @@ int or_ray(const or_sensor *se, int32_t col, int32_t row, double nu[3], double n
         nu[0] = sp; nu[1] = -cp; nu[2] = 0.0;
         nv[0] = ct * cp; nv[1] = ct * sp; nv[2] = -st;
         return td <= tdmax;
+    }
+    if (se->kind == OR_CYLINDRICAL) {
+        /* Eq. 4, reading R20: phi = (p_x - c_x)/f_x is the azimuth
+         * about the camera y axis and h_u = (cos phi, 0, -sin phi, 0) verbatim;
+         * h_v = (0, -1, 0, p_y) read in the cylindrical screen space whose
+         * homogeneous coordinate is rho = sin(phi) x + cos(phi) z (K folded, as
+         * in Eq. 3): -(f_y y + c_y rho) + p_y rho = 0, i.e. the plane
+         * -y + yh rho = 0 with yh = (p_y - c_y)/f_y.  Ray: (sin phi, yh, cos phi),
+         * normalised (ray parameter = range). */
+        const double ph = (p[0] - se->cx) / se->fx, yh = (p[1] - se->cy) / se->fy;
+        const double sf = sin(ph), cf = cos(ph), nd = sqrt(1.0 + yh * yh);
+        nu[0] = cf; nu[1] = 0.0; nu[2] = -sf;
+        nv[0] = yh * sf; nv[1] = -1.0; nv[2] = yh * cf;
+        d[0] = sf / nd; d[1] = yh / nd; d[2] = cf / nd;
+        return 1;
     }
     /* LiDAR, Eq. 5 with theta = elevation, phi = azimuth (reading R5) */
     const double th = se->beam_elevation[row];

@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-enum { OR_PINHOLE = 0, OR_FISHEYE = 1, OR_LIDAR = 2 };
+enum { OR_PINHOLE = 0, OR_FISHEYE = 1, OR_LIDAR = 2, OR_CYLINDRICAL = 3 };
 
 typedef struct {
     int64_t n;

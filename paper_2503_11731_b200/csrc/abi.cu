@@ -92,7 +92,7 @@ static gs_status check_opts(const gs_opts *o) {
 
 static gs_status check_sensor(const gs_sensor *s) {
     if (!s) return fail(GS_ERR_CONFIG, "sensor is NULL");
-    if (s->kind < 0 || s->kind > 2) return fail(GS_ERR_CONFIG, "unknown sensor kind");
+    if (s->kind < 0 || s->kind > 3) return fail(GS_ERR_CONFIG, "unknown sensor kind");
     if (s->width < 1 || s->height < 1) return fail(GS_ERR_CONFIG, "width/height < 1");
     // pixel boxes are packed as two u16 pairs (0xffff = empty); LiDAR column
     // bounds run to 2W-1 across the azimuth seam
@@ -103,6 +103,11 @@ static gs_status check_sensor(const gs_sensor *s) {
     if (s->kind != GS_LIDAR_SPINNING) {
         if (!(s->fx > 0.f) || !(s->fy > 0.f)) return fail(GS_ERR_RANGE, "focal length must be > 0");
         if (!std::isfinite(s->cx) || !std::isfinite(s->cy)) return fail(GS_ERR_RANGE, "principal point not finite");
+        if (s->kind == GS_FISHEYE_CYLINDRICAL) {
+            // the columns' azimuths (p_x - c_x) / f_x, p_x in [0, W], must lie in [-pi, pi]
+            if (!((double)s->cx / (double)s->fx <= M_PI && ((double)s->width - (double)s->cx) / (double)s->fx <= M_PI))
+                return fail(GS_ERR_RANGE, "cylindrical image spans azimuths outside [-pi, pi]");
+        }
         if (s->kind == GS_FISHEYE_EQUIDISTANT) {
             if (!(s->theta_max > 0.f && s->theta_max < (float)M_PI))
                 return fail(GS_ERR_RANGE, "theta_max outside (0, pi)");

@@ -81,8 +81,14 @@ __host__ __device__ inline float pack_bb(int lo, int hi) {
 #endif
 }
 
+// cameras whose rays are unit directions through the optical centre (records
+// relative to the centre direction): equidistant and cylindrical fisheye
+__host__ __device__ constexpr bool dir_camera(int kind) {
+    return kind == GS_FISHEYE_EQUIDISTANT || kind == GS_FISHEYE_CYLINDRICAL;
+}
+
 __host__ __device__ inline int record_floats(int kind) {
-    return kind == GS_PINHOLE ? (int)PH_FLOATS : (kind == GS_FISHEYE_EQUIDISTANT ? (int)FE_FLOATS : (int)LI_FLOATS);
+    return kind == GS_PINHOLE ? (int)PH_FLOATS : (dir_camera(kind) ? (int)FE_FLOATS : (int)LI_FLOATS);
 }
 
 // ---------------------------------------------------------------- projected buffer

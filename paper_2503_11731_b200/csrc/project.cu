@@ -60,6 +60,16 @@ __device__ __forceinline__ void fisheye_project(const DevSensor &se, const doubl
     }
 }
 
+// cylindrical projection (Eq. 4, reading R20) of a sensor-frame point: column
+// from the azimuth about the camera y axis, row from y / sqrt(x^2 + z^2)
+__device__ __forceinline__ void cylinder_project(const DevSensor &se, const double m[3], double &px,
+                                                 double &py) {
+    const double rho = sqrt(m[0] * m[0] + m[2] * m[2]);
+    px = (double)se.cx + (double)se.fx * atan2(m[0], m[2]);
+    const double t = rho > 0.0 ? m[1] / rho : (m[1] >= 0.0 ? 1e12 : -1e12);
+    py = (double)se.cy + (double)se.fy * fmin(fmax(t, -1e12), 1e12);
+}
+
 // Pixel-space bound of the pinhole 3-sigma disk clipped to z >= near:
 // extremes of the linear-fractional x = X/Z over {u^2+v^2 <= R^2, Z >= near}
 // lie at the circle's stationary points (A c + B s + C = 0) or at the ends of
@@ -404,6 +414,7 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
         if ((yr * Z - Y) < -R * sqrtf(1.f + yr * yr)) return false;
         return true;
     }
+    if (KIND == GS_FISHEYE_CYLINDRICAL) return true;   // no field-of-view pre-cull: k_project's box decides
     const float r = sqrtf(X * X + Y * Y + Z * Z);
     if (!(r > R * 1.01f)) return true;
     if (KIND == GS_FISHEYE_EQUIDISTANT) {
@@ -594,9 +605,17 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             if (!whole) {
                 double a[3], b[3];
                 for (int k = 0; k < 3; ++k) { a[k] = Rr * su * A[k]; b[k] = Rr * sv * Bv[k]; }
-                const bool fast = KIND == GS_LIDAR_SPINNING && angular_box_disk_f(mu, a, b, ab);
-                if (!fast && !angular_box_disk(mu, a, b, ab, KIND == GS_FISHEYE_EQUIDISTANT))
-                    angular_box_cap(m, asin(R3 / r), ab);
+                if (KIND == GS_FISHEYE_CYLINDRICAL) {
+                    // azimuth about the camera y axis and elevation from the xz plane: the
+                    // LiDAR-style box of the cyclically permuted frame (z, x, y)
+                    const double mp[3] = {mu[2], mu[0], mu[1]}, ap[3] = {a[2], a[0], a[1]},
+                                 bp[3] = {b[2], b[0], b[1]}, up[3] = {m[2], m[0], m[1]};
+                    if (!angular_box_disk(mp, ap, bp, ab, true)) angular_box_cap(up, asin(R3 / r), ab);
+                } else {
+                    const bool fast = KIND == GS_LIDAR_SPINNING && angular_box_disk_f(mu, a, b, ab);
+                    if (!fast && !angular_box_disk(mu, a, b, ab, KIND == GS_FISHEYE_EQUIDISTANT))
+                        angular_box_cap(m, asin(R3 / r), ab);
+                }
             }
             if (KIND == GS_FISHEYE_EQUIDISTANT) {
                 Box bx;
@@ -635,6 +654,42 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
                 }
                 double cxp, cyp;
                 fisheye_project(se, mu, cxp, cyp);
+                bx.add(cxp - rlp, cyp - rlp);
+                bx.add(cxp + rlp, cyp + rlp);
+                vis = box_to_tiles(bx, se.width, se.height, se.mtw, se.mth, tx0, ty0, tx1, ty1, pb);
+            } else if (KIND == GS_FISHEYE_CYLINDRICAL) {
+                Box bx;
+                bx.init();
+                if (whole) {
+                    bx.add(0.f, 0.f);
+                    bx.add((float)se.width, (float)se.height);
+                } else {
+                    // rows: y / rho = tan(elevation), monotone
+                    const double lim = 1e9;
+                    const double tlo = ab.el_lo <= -0.5 * M_PI + 1e-12 ? -lim : fmax(tan(ab.el_lo), -lim);
+                    const double thi = ab.el_hi >= 0.5 * M_PI - 1e-12 ? lim : fmin(tan(ab.el_hi), lim);
+                    const double y0 = (double)se.cy + (double)se.fy * tlo, y1 = (double)se.cy + (double)se.fy * thi;
+                    // columns: the azimuth interval (and its shifts by 2 pi) inside the image's
+                    // azimuth range [-c_x / f_x, (W - c_x) / f_x] (within [-pi, pi], gsr.h)
+                    const double ilo = -(double)se.cx / (double)se.fx;
+                    const double ihi = ((double)se.width - (double)se.cx) / (double)se.fx;
+                    double lo = 1e30, hi = -1e30;
+                    if (ab.all_az) {
+                        lo = ilo; hi = ihi;
+                    } else {
+                        for (int kk = -1; kk <= 1; ++kk) {
+                            const double a0 = fmax(ab.azc + ab.daz_lo + kk * 2.0 * M_PI, ilo);
+                            const double a1 = fmin(ab.azc + ab.daz_hi + kk * 2.0 * M_PI, ihi);
+                            if (a0 <= a1) { lo = fmin(lo, a0); hi = fmax(hi, a1); }
+                        }
+                    }
+                    if (lo <= hi) {
+                        bx.add((float)((double)se.cx + (double)se.fx * lo), (float)y0);
+                        bx.add((float)((double)se.cx + (double)se.fx * hi), (float)y1);
+                    }
+                }
+                double cxp, cyp;
+                cylinder_project(se, mu, cxp, cyp);
                 bx.add(cxp - rlp, cyp - rlp);
                 bx.add(cxp + rlp, cyp + rlp);
                 vis = box_to_tiles(bx, se.width, se.height, se.mtw, se.mth, tx0, ty0, tx1, ty1, pb);
@@ -755,7 +810,7 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         for (int k = 0; k < PH_FLOATS / 4; ++k)
             dst[k] = make_float4(R[4 * k], R[4 * k + 1], R[4 * k + 2], R[4 * k + 3]);
     } else {
-        constexpr int NF = KIND == GS_FISHEYE_EQUIDISTANT ? FE_FLOATS : LI_FLOATS;
+        constexpr int NF = dir_camera(KIND) ? FE_FLOATS : LI_FLOATS;
         float R[NF];
 #pragma unroll
         for (int k = 0; k < NF; ++k) R[k] = 0.f;
@@ -777,9 +832,10 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
         R[RY_RCUT3] = rcut3;
         R[RY_O] = o;
         R[RY_RC] = (float)r;
-        if (KIND == GS_FISHEYE_EQUIDISTANT) {
+        if (dir_camera(KIND)) {
             double cxp, cyp;
-            fisheye_project(se, mu, cxp, cyp);
+            if (KIND == GS_FISHEYE_EQUIDISTANT) fisheye_project(se, mu, cxp, cyp);
+            else cylinder_project(se, mu, cxp, cyp);
             split_hilo(cxp, R[FE_CHX], R[FE_CLX]);
             split_hilo(cyp, R[FE_CHY], R[FE_CLY]);
             R[FE_RCUT2] = rcut3 * op.sigma2;
@@ -931,6 +987,8 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_PINHOLE>, 256, 0);
     else if (se.kind == GS_FISHEYE_EQUIDISTANT)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_FISHEYE_EQUIDISTANT>, 256, 0);
+    else if (se.kind == GS_FISHEYE_CYLINDRICAL)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_FISHEYE_CYLINDRICAL>, 256, 0);
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_project<GS_LIDAR_SPINNING>, 256, 0);
     const unsigned gp = (unsigned)std::min<int64_t>((s.n + 255) / 256, (int64_t)nsm * std::max(occ, 1));
@@ -941,6 +999,9 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     } else if (se.kind == GS_FISHEYE_EQUIDISTANT) {
         k_cull<GS_FISHEYE_EQUIDISTANT><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_FISHEYE_EQUIDISTANT><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
+    } else if (se.kind == GS_FISHEYE_CYLINDRICAL) {
+        k_cull<GS_FISHEYE_CYLINDRICAL><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
+        k_project<GS_FISHEYE_CYLINDRICAL><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);
     } else {
         k_cull<GS_LIDAR_SPINNING><<<nblk, SCAN_THREADS, 0, st>>>(s, se, op, rect, key, cnt, cand, stc, hdr);
         k_project<GS_LIDAR_SPINNING><<<gp, 256, 0, st>>>(s, se, op, cand, hdr, rec, rect, key, cnt);

@@ -66,6 +66,7 @@ template <int KIND> struct Rec;
 template <> struct Rec<GS_PINHOLE> { static constexpr int F = PH_FLOATS, BB = PH_BBX, S4 = PH_FLOATS / 4; };
 template <> struct Rec<GS_FISHEYE_EQUIDISTANT> { static constexpr int F = FE_FLOATS, BB = FE_BBX, S4 = FE_FLOATS / 4; };
 template <> struct Rec<GS_LIDAR_SPINNING> { static constexpr int F = LI_FLOATS, BB = LI_BBX, S4 = LI_FLOATS / 4; };
+template <> struct Rec<GS_FISHEYE_CYLINDRICAL> : Rec<GS_FISHEYE_EQUIDISTANT> {};
 
 // ---------------------------------------------------------------- workspace
 struct SchedHdr {
@@ -186,6 +187,18 @@ __device__ __forceinline__ Ray make_ray(const DevSensor &se, const SubTile &st, 
         split_hilo(st_ * cp, ry.dh[0], ry.dl[0]);
         split_hilo(st_ * sp, ry.dh[1], ry.dl[1]);
         split_hilo(ct, ry.dh[2], ry.dl[2]);
+    }
+    if (KIND == GS_FISHEYE_CYLINDRICAL && ry.inside) {
+        // Eq. 4 (reading R20): column -> azimuth phi about the camera y axis, row ->
+        // y / sqrt(x^2 + z^2) = (p_y - c_y) / f_y; unit ray (sin phi, yh, cos phi) / sqrt(1 + yh^2)
+        const double ph = __ddiv_rn(__dadd_rn((double)ry.px, -(double)se.cx), (double)se.fx);
+        const double yh = __ddiv_rn(__dadd_rn((double)ry.py, -(double)se.cy), (double)se.fy);
+        double sp, cp;
+        sincos(ph, &sp, &cp);
+        const double inv = 1.0 / sqrt(1.0 + yh * yh);
+        split_hilo(sp * inv, ry.dh[0], ry.dl[0]);
+        split_hilo(yh * inv, ry.dh[1], ry.dl[1]);
+        split_hilo(cp * inv, ry.dh[2], ry.dl[2]);
     }
     if (KIND == GS_LIDAR_SPINNING && ry.inside) {   // Eq. 5: theta = elevation (row), phi = azimuth (column)
         const double th = (double)se.beam[ry.pyi];
@@ -325,7 +338,7 @@ __device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const 
         const float hv = fmaf(g3.x, ex, fmaf(g3.y, ey, g3.z * ez));
         const float Dd = fmaf(g4.x, ex, fmaf(g4.y, ey, fmaf(g4.z, ez, g1.w)));
         const float n3 = fmaf(hu, hu, hv * hv);
-        if (KIND == GS_FISHEYE_EQUIDISTANT) {
+        if (dir_camera(KIND)) {
             const float4 g5 = r[5], g6 = r[6];
             const float dx = (ry.px - g5.x) - g5.z, dy = (ry.py - g5.y) - g5.w;
             const float s2 = fmaf(dx, dx, dy * dy);
@@ -1077,6 +1090,9 @@ cudaError_t launch_render_camera(const void *proj, int64_t n, const uint32_t *va
     if (se.kind == GS_PINHOLE)
         return stats ? launch<GS_PINHOLE, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st)
                      : launch<GS_PINHOLE, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st);
+    if (se.kind == GS_FISHEYE_CYLINDRICAL)
+        return stats ? launch<GS_FISHEYE_CYLINDRICAL, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st)
+                     : launch<GS_FISHEYE_CYLINDRICAL, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st);
     return stats ? launch<GS_FISHEYE_EQUIDISTANT, true>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st)
                  : launch<GS_FISHEYE_EQUIDISTANT, false>(proj, n, values, ranges, d_overflow, se, op, split_len, ws, ws_bytes, rgb, depth, normal, alpha, stats, st);
 }

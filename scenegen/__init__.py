@@ -29,6 +29,7 @@ import numpy as np
 PINHOLE = 0
 FISHEYE = 1
 LIDAR = 2
+CYLINDRICAL = 3
 
 SH_C0 = 0.28209479177387814  # only used to encode Tiny's uniform RGB as a DC coefficient
 
@@ -164,6 +165,16 @@ def fisheye(width, height, theta_max, k, cx, cy, pose) -> Sensor:
     f = (width / 2.0) / tdm
     return Sensor(FISHEYE, int(width), int(height), pose, fx=float(_f32(f)), fy=float(_f32(f)),
                   cx=float(_f32(cx)), cy=float(_f32(cy)), k=k, theta_max=float(_f32(theta_max)))
+
+
+def cylindrical(width, height, hfov, vfov, pose, cx=None, cy=None) -> Sensor:
+    """Cylindrical fisheye (Eq. 4): the columns span the horizontal
+    field of view hfov (f_x = W / hfov, azimuth (p_x - c_x)/f_x), the rows span
+    y / sqrt(x^2 + z^2) in +-tan(vfov / 2) (f_y = (H/2) / tan(vfov/2))."""
+    fx = width / hfov
+    fy = (height / 2.0) / math.tan(vfov / 2.0)
+    return Sensor(CYLINDRICAL, int(width), int(height), pose, fx=float(_f32(fx)), fy=float(_f32(fy)),
+                  cx=float(_f32(width / 2.0 if cx is None else cx)), cy=float(_f32(height / 2.0 if cy is None else cy)))
 
 
 # --------------------------------------------------------------------------- surfels

@@ -33,6 +33,24 @@ def test_eq5_lidar_planes_paper_value():
     np.testing.assert_allclose(d, [1, 0, 0], atol=0)
 
 
+def test_eq4_cylindrical_planes_paper_value():
+    """PAPER value: Eq. 4's h_u = (cos phi, 0, -sin phi, 0) at phi = 0 and
+    phi = pi/2, and h_v at the principal row (golden/eq4_cylindrical_planes.json)."""
+    g = golden("eq4_cylindrical_planes.json")
+    se = sg.cylindrical(33, 25, np.deg2rad(120), np.deg2rad(60), sg.identity_pose(), cx=16.5, cy=12.5)
+    nu, nv, d, p, ok = oracle.ray(se, 16, 12)
+    assert ok and p[0] == 16.5 and p[1] == 12.5
+    np.testing.assert_array_equal(nu, g["h_u_phi0"][:3])
+    np.testing.assert_array_equal(nv, g["h_v_centre"][:3])
+    np.testing.assert_allclose(d, [0, 0, 1], atol=0)
+    # a column a quarter turn to the right: phi = pi/2
+    se2 = sg.Sensor(sg.CYLINDRICAL, 33, 25, sg.identity_pose(), fx=1.0, fy=1.0,
+                    cx=float(np.float32(16.5 - np.pi / 2)), cy=12.5)
+    nu, nv, d, _, _ = oracle.ray(se2, 16, 12)
+    np.testing.assert_allclose(nu, g["h_u_phi_half_pi"][:3], atol=1e-6)
+    np.testing.assert_allclose(d, [1, 0, 0], atol=1e-6)
+
+
 def test_eq3_pinhole_planes_paper_value():
     """Eq. 3 at the principal point (golden/eq3_pinhole_planes.json)."""
     g = golden("eq3_pinhole_planes.json")
@@ -48,10 +66,11 @@ def _sensors_for_planes():
     k, _ = sg.draw_fisheye_k(rng, float(np.float32(np.deg2rad(95))))
     return [sg.pinhole(64, 48, 40.0, 30.0, 26.0, sg.identity_pose()),
             sg.fisheye(64, 48, np.deg2rad(95), k, 32.0, 24.0, sg.identity_pose()),
-            small_lidar(16, 128, 15.0, -25.0)]
+            small_lidar(16, 128, 15.0, -25.0),
+            sg.cylindrical(96, 40, np.deg2rad(300), np.deg2rad(100), sg.identity_pose(), cx=41.0, cy=17.0)]
 
 
-@pytest.mark.parametrize("si", [0, 1, 2])
+@pytest.mark.parametrize("si", [0, 1, 2, 3])
 def test_plane_pairs_contain_the_ray(si):
     """Closed form: both planes contain the ray (n.d = 0) and n_u x n_v || d;
     the pinhole/LiDAR direction reprojects to the sample coordinate."""
@@ -69,6 +88,10 @@ def test_plane_pairs_contain_the_ray(si):
         if se.kind == sg.PINHOLE:  # reproject d through K
             assert abs(se.fx * d[0] / d[2] + se.cx - p[0]) < 1e-9
             assert abs(se.fy * d[1] / d[2] + se.cy - p[1]) < 1e-9
+        elif se.kind == sg.CYLINDRICAL:  # Eq. 4: azimuth about y, height over the y-axis distance
+            assert abs(se.cx + se.fx * math.atan2(d[0], d[2]) - p[0]) < 1e-9
+            assert abs(se.cy + se.fy * d[1] / math.hypot(d[0], d[2]) - p[1]) < 1e-9
+            assert abs(np.linalg.norm(d) - 1.0) < 1e-14
         elif se.kind == sg.LIDAR:  # elevation / azimuth of d (reading R5: theta = elevation)
             assert abs(math.asin(d[2]) - float(se.beam_elevation[row])) < 1e-12
             ph = se.azimuth0 + col * se.azimuth_step
@@ -444,7 +467,8 @@ def test_random_small_scenes_all_sensors_match_naive(seed):
     k, _ = sg.draw_fisheye_k(rng, float(np.float32(np.deg2rad(95))))
     for se in [sg.pinhole(16, 16, 10.0, 8.0, 8.0, sg.identity_pose()),
                sg.fisheye(16, 16, np.deg2rad(95), k, 8.0, 8.0, sg.identity_pose()),
-               small_lidar(16, 32, 30.0, -30.0)]:
+               small_lidar(16, 32, 30.0, -30.0),
+               sg.cylindrical(24, 12, np.deg2rad(330), np.deg2rad(110), sg.identity_pose())]:
         a, _, _ = oracle.render(s, se)
         b = naive.render(s, se)
         assert np.abs(a - b).max() < 1e-10
