@@ -297,6 +297,48 @@ gs_status gs_decode_anchors(const gs_anchors *anchors, const gs_decoder *decoder
                             float *means, float *quats, float *scales, float *opacities, float *sh,
                             float *intensity, float *raydrop_logit, gs_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Pixel-partitioned rendering of one frame over several GPUs (SURVEY.md
+ * §8(f) NEXT-4; §III-A "Paralleled training": continuous
+ * image regions per GPU and "a sparse all-to-all communication scheme to
+ * transfer the required Gaussian data to corresponding pixel partitions").
+ * Each rank owns a contiguous shard of the surfels and one band of tile
+ * rows.  A rank projects its shard for the frame (gs_project), routes every
+ * visible surfel to the bands its tile rect overlaps (gs_band_route), packs
+ * the routed surfels' attributes per band (gs_pack_surfels) for the
+ * all-to-all, and renders its band from the received surfels (unpacked in
+ * source-rank order = global index order, so depth ties keep their order)
+ * with the band's cropped sensor (paper_2503_11731_b200/pixdist.py).
+ */
+#define GS_MAX_BANDS 64
+
+size_t gs_band_route_workspace_bytes(int64_t n, int32_t n_bands);
+
+/* band_rows: HOST [n_bands+1] tile-row boundaries, band_rows[0] = 0 <
+ * band_rows[1] < ... < band_rows[n_bands] = tile rows of the sensor under
+ * opts.  d_counts: device [n_bands] u32 (out): surfels routed to each band.
+ * d_index: device [n_bands, n] u32 (out): band b's surfel indices, ascending,
+ * in d_index[b*n .. b*n + d_counts[b]).  GS_ERR_RANGE for a bad band table. */
+gs_status gs_band_route(const void *projected, int64_t n, const gs_sensor *sensor, const gs_opts *opts,
+                        const int32_t *band_rows, int32_t n_bands, uint32_t *d_counts, uint32_t *d_index,
+                        void *workspace, size_t workspace_bytes, gs_stream stream);
+
+/* floats per packed surfel: mean 3, quat 4, scale 2, opacity 1, SH
+ * (sh_degree+1)^2*3 (sh_degree < 0: none), intensity 1 and ray-drop logit 1
+ * if present */
+int32_t gs_payload_floats(int32_t sh_degree, int32_t has_intensity, int32_t has_raydrop);
+
+/* payload [m, gs_payload_floats] (device, out) <- the attributes of surfels
+ * d_index[0..m) of src; src->sh may be NULL (no SH packed) */
+gs_status gs_pack_surfels(const gs_surfels *src, const uint32_t *d_index, int64_t m, float *payload,
+                          gs_stream stream);
+
+/* device SoA arrays (out, [m,...]) <- payload [m, gs_payload_floats]; sh,
+ * intensity and raydrop_logit are written only if present in the payload */
+gs_status gs_unpack_surfels(const float *payload, int64_t m, int32_t sh_degree, int32_t has_intensity,
+                            int32_t has_raydrop, float *means, float *quats, float *scales, float *opacities,
+                            float *sh, float *intensity, float *raydrop_logit, gs_stream stream);
+
 const char *gs_status_string(gs_status status);
 const char *gs_last_error(void);
 

@@ -17,6 +17,15 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
                             int32_t *d_overflow, cudaStream_t st);
 size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix);
+size_t band_route_workspace_bytes(int64_t n, int32_t nb);
+cudaError_t launch_band_route(const void *proj, int64_t n, int kind, const int32_t *band_rows, int32_t nb,
+                              uint32_t *d_counts, uint32_t *d_index, void *ws, cudaStream_t st);
+int32_t payload_floats(int sh_floats, int has_int, int has_drop);
+cudaError_t launch_pack(const DevSurfels &s, int sh_floats, const uint32_t *index, int64_t m, float *out,
+                        cudaStream_t st);
+cudaError_t launch_unpack(const float *in, int64_t m, int sh_floats, int has_int, int has_drop, float *means,
+                          float *quats, float *scales, float *opac, float *sh, float *inten, float *drop,
+                          cudaStream_t st);
 cudaError_t launch_decode(const gs_anchors *, const gs_decoder *, const float[3], float *, float *, float *,
                           float *, float *, float *, float *, cudaStream_t);
 cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
@@ -367,6 +376,70 @@ extern "C" gs_status gs_decode_anchors(const gs_anchors *an, const gs_decoder *d
                                         raydrop_logit, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_decode_anchors");
     return GS_OK;
+}
+
+extern "C" size_t gs_band_route_workspace_bytes(int64_t n, int32_t n_bands) {
+    return band_route_workspace_bytes(n, n_bands < 1 ? 1 : n_bands);
+}
+
+extern "C" gs_status gs_band_route(const void *projected, int64_t n, const gs_sensor *s, const gs_opts *o,
+                                   const int32_t *band_rows, int32_t n_bands, uint32_t *d_counts,
+                                   uint32_t *d_index, void *workspace, size_t workspace_bytes, gs_stream stream) {
+    gs_status st = check_sensor(s);
+    if (st != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if (n < 0) return fail(GS_ERR_CONFIG, "n < 0");
+    if (!band_rows || n_bands < 1 || n_bands > GS_MAX_BANDS) return fail(GS_ERR_RANGE, "band table: 1..GS_MAX_BANDS bands");
+    const int32_t ty = (s->height + o->tile_h - 1) / o->tile_h;
+    if (band_rows[0] != 0 || band_rows[n_bands] != ty) return fail(GS_ERR_RANGE, "band table must cover the tile rows");
+    for (int b = 0; b < n_bands; ++b)
+        if (!(band_rows[b + 1] > band_rows[b])) return fail(GS_ERR_RANGE, "band table not strictly increasing");
+    if (!d_counts || (n > 0 && (!projected || !d_index || !workspace)))
+        return fail(GS_ERR_CONFIG, "NULL buffer");
+    if (workspace_bytes < band_route_workspace_bytes(n, n_bands)) return fail(GS_ERR_CONFIG, "workspace too small");
+    if (n == 0) {
+        const cudaError_t e = cudaMemsetAsync(d_counts, 0, 4 * (size_t)n_bands, (cudaStream_t)stream);
+        return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_band_route");
+    }
+    const cudaError_t e = launch_band_route(projected, n, s->kind, band_rows, n_bands, d_counts, d_index, workspace,
+                                            (cudaStream_t)stream);
+    return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_band_route");
+}
+
+extern "C" int32_t gs_payload_floats(int32_t sh_degree, int32_t has_intensity, int32_t has_raydrop) {
+    const int nsh = sh_degree < 0 ? 0 : (sh_degree + 1) * (sh_degree + 1) * 3;
+    return payload_floats(nsh, has_intensity != 0, has_raydrop != 0);
+}
+
+extern "C" gs_status gs_pack_surfels(const gs_surfels *src, const uint32_t *d_index, int64_t m, float *payload,
+                                     gs_stream stream) {
+    if (!src || m < 0) return fail(GS_ERR_CONFIG, "src is NULL or m < 0");
+    if (m == 0) return GS_OK;
+    if (!d_index || !payload || !src->means || !src->quats || !src->scales || !src->opacities)
+        return fail(GS_ERR_CONFIG, "NULL buffer");
+    if (src->sh && (src->sh_degree < 0 || src->sh_degree > 3)) return fail(GS_ERR_CONFIG, "sh_degree outside 0..3");
+    DevSurfels d;
+    d.n = src->n; d.means = src->means; d.quats = src->quats; d.scales = src->scales; d.opac = src->opacities;
+    d.sh = src->sh; d.sh_degree = src->sh_degree; d.inten = src->intensity; d.drop = src->raydrop_logit;
+    const int nsh = src->sh ? (src->sh_degree + 1) * (src->sh_degree + 1) * 3 : 0;
+    const cudaError_t e = launch_pack(d, nsh, d_index, m, payload, (cudaStream_t)stream);
+    return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_pack_surfels");
+}
+
+extern "C" gs_status gs_unpack_surfels(const float *payload, int64_t m, int32_t sh_degree, int32_t has_intensity,
+                                       int32_t has_raydrop, float *means, float *quats, float *scales,
+                                       float *opacities, float *sh, float *intensity, float *raydrop_logit,
+                                       gs_stream stream) {
+    if (m < 0) return fail(GS_ERR_CONFIG, "m < 0");
+    if (m == 0) return GS_OK;
+    if (sh_degree > 3) return fail(GS_ERR_CONFIG, "sh_degree outside 0..3");
+    if (!payload || !means || !quats || !scales || !opacities || (sh_degree >= 0 && !sh) ||
+        (has_intensity && !intensity) || (has_raydrop && !raydrop_logit))
+        return fail(GS_ERR_CONFIG, "NULL buffer");
+    const int nsh = sh_degree < 0 ? 0 : (sh_degree + 1) * (sh_degree + 1) * 3;
+    const cudaError_t e = launch_unpack(payload, m, nsh, has_intensity != 0, has_raydrop != 0, means, quats, scales,
+                                        opacities, sh, intensity, raydrop_logit, (cudaStream_t)stream);
+    return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_unpack_surfels");
 }
 
 extern "C" const char *gs_status_string(gs_status s) {

@@ -69,7 +69,8 @@ class gs_decoder(C.Structure):
     _fields_ = [("modality", C.c_int32), ("head", gs_mlp * 6)]
 
 
-EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
+EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_band_route_workspace_bytes", "gs_band_route",
+           "gs_payload_floats", "gs_pack_surfels", "gs_unpack_surfels", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
            "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes",
            "gs_kernel_launches"]
@@ -122,6 +123,16 @@ def load(build_if_missing: bool = True):
     lib.gs_last_error.restype = C.c_char_p
     lib.gs_decode_anchors.argtypes = [P(gs_anchors), P(gs_decoder), vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.gs_decode_anchors.restype = C.c_int
+    lib.gs_band_route_workspace_bytes.argtypes = [C.c_int64, C.c_int32]
+    lib.gs_band_route_workspace_bytes.restype = C.c_size_t
+    lib.gs_band_route.argtypes = [vp, C.c_int64, P(gs_sensor), P(gs_opts), vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]
+    lib.gs_band_route.restype = C.c_int
+    lib.gs_payload_floats.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+    lib.gs_payload_floats.restype = C.c_int32
+    lib.gs_pack_surfels.argtypes = [P(gs_surfels), vp, C.c_int64, vp, vp]
+    lib.gs_pack_surfels.restype = C.c_int
+    lib.gs_unpack_surfels.argtypes = [vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.gs_unpack_surfels.restype = C.c_int
     lib.gs_kernel_launches.argtypes = []
     lib.gs_kernel_launches.restype = C.c_uint64
     _lib = lib
@@ -253,6 +264,33 @@ def gs_decode_anchors(anchors: gs_anchors, decoder: gs_decoder, view_origin, mea
     _check(load().gs_decode_anchors(C.byref(anchors), C.byref(decoder), origin, _ptr(means), _ptr(quats),
                                     _ptr(scales), _ptr(opacities), _ptr(sh), _ptr(intensity),
                                     _ptr(raydrop_logit), C.c_void_p(stream)))
+
+
+def gs_band_route_workspace_bytes(n, n_bands):
+    return int(load().gs_band_route_workspace_bytes(int(n), int(n_bands)))
+
+
+def gs_band_route(projected, n, sensor: Sensor, opts: gs_opts, band_rows, d_counts, d_index, workspace, stream):
+    rows = np.ascontiguousarray(band_rows, np.int32)
+    _check(load().gs_band_route(_ptr(projected), int(n), sensor.ref, C.byref(opts), rows.ctypes.data,
+                                int(len(rows) - 1), _ptr(d_counts), _ptr(d_index), _ptr(workspace),
+                                workspace.numel() * workspace.element_size(), C.c_void_p(stream)))
+
+
+def gs_payload_floats(sh_degree, has_intensity, has_raydrop):
+    return int(load().gs_payload_floats(int(sh_degree), int(bool(has_intensity)), int(bool(has_raydrop))))
+
+
+def gs_pack_surfels(src: gs_surfels, d_index, m, payload, stream):
+    _check(load().gs_pack_surfels(C.byref(src), _ptr(d_index), int(m), _ptr(payload), C.c_void_p(stream)))
+
+
+def gs_unpack_surfels(payload, m, sh_degree, has_intensity, has_raydrop, means, quats, scales, opacities, sh,
+                      intensity, raydrop_logit, stream):
+    _check(load().gs_unpack_surfels(_ptr(payload), int(m), int(sh_degree), int(bool(has_intensity)),
+                                    int(bool(has_raydrop)), _ptr(means), _ptr(quats), _ptr(scales),
+                                    _ptr(opacities), _ptr(sh), _ptr(intensity), _ptr(raydrop_logit),
+                                    C.c_void_p(stream)))
 
 
 def gs_kernel_launches() -> int:

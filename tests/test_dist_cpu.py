@@ -4,6 +4,7 @@ world_size-2 (and 3) gloo process group."""
 import os
 import socket
 
+import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -197,3 +198,68 @@ def test_bench_step_bookkeeping_world4_gloo(world, n_t, schedule):
         p.join(timeout=60)
     assert res[0] == "ok" and res[1], res
     assert all(p.exitcode == 0 for p in ps)
+
+
+# ---------------------------------------------------------------- pixel-partitioned frame (NEXT-4)
+def test_balanced_and_adaptive_bands():
+    from paper_2503_11731_b200 import pixdist as pd
+    assert pd.balanced_bands(np.ones(16), 4) == [0, 4, 8, 12, 16]
+    b = pd.balanced_bands([0, 0, 10, 0, 0, 0, 0, 10], 2)
+    assert b[0] == 0 and b[-1] == 8 and 2 < b[1] <= 7
+    for nb in (1, 3, 8):   # every band keeps >= 1 row even with all cost in one row
+        b = pd.balanced_bands([0] * 10 + [5] + [0] * 5, nb)
+        assert len(b) == nb + 1 and all(b[i + 1] > b[i] for i in range(nb)) and b[-1] == 16
+    # time-adaptive: band 0 took 3x longer per pair -> its boundary moves up
+    pairs = np.ones(20)
+    nb = pd.adapt_bands([0, 10, 20], [30.0, 10.0], pairs)
+    assert nb[1] < 10
+    # equal measured cost -> unchanged
+    assert pd.adapt_bands([0, 10, 20], [10.0, 10.0], pairs) == [0, 10, 20]
+
+
+def _pix_worker(rank, world, port, q):
+    """The sparse all-to-all of pixdist.exchange on gloo: each rank routes its
+    shard of synthetic tile rects to bands brute force, sends the routed rows
+    (global index, a payload value), and must receive exactly the overlap set
+    of its band in ascending global order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    try:
+        from paper_2503_11731_b200 import pixdist as pd
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        n, rows = 997, 23
+        g = torch.Generator().manual_seed(7)
+        y0 = torch.randint(0, rows, (n,), generator=g)
+        y1 = torch.clamp(y0 + torch.randint(0, 6, (n,), generator=g), max=rows - 1)
+        vis = torch.rand(n, generator=g) < 0.8
+        bounds = pd.balanced_bands(np.ones(rows), world)
+        lo, hi = gd.shard_range(n, world, rank)
+        rows_out, counts = [], []
+        for b in range(world):
+            sel = [i for i in range(lo, hi) if vis[i] and y1[i] >= bounds[b] and y0[i] < bounds[b + 1]]
+            rows_out += [[float(i), float(i) * 0.5] for i in sel]
+            counts.append(len(sel))
+        payload = torch.tensor(rows_out, dtype=torch.float32).reshape(-1, 2)
+        recv, rc = pd.exchange(payload, counts)
+        want = [i for i in range(n) if vis[i] and y1[i] >= bounds[rank] and y0[i] < bounds[rank + 1]]
+        ok = recv[:, 0].to(torch.int64).tolist() == want and torch.equal(recv[:, 1], recv[:, 0] * 0.5)
+        ok = ok and sum(rc) == len(want)
+        q.put(("ok", bool(ok), rank))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), rank))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pixel_partition_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_pix_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[0] == "ok" and r[1] for r in res), res
