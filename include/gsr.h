@@ -339,6 +339,34 @@ gs_status gs_unpack_surfels(const float *payload, int64_t m, int32_t sh_degree, 
                             int32_t has_raydrop, float *means, float *quats, float *scales, float *opacities,
                             float *sh, float *intensity, float *raydrop_logit, gs_stream stream);
 
+/* ------------------------------------------------------------------------
+ * gs_render_backward -- backward pass of the compositing (SURVEY.md §8(f)
+ * NEXT-2; training: PAPER.md:167, :214): the gradients of
+ *     L = sum_{channel c, sample p} grad_out[c, p] * out[c, p]
+ * (out = the frame gs_render_camera / gs_render_lidar produces: camera
+ * r,g,b,depth,nx,ny,nz,alpha; LiDAR range,intensity,raydrop,alpha) with
+ * respect to the surfel attributes, for GS_PINHOLE and GS_LIDAR_SPINNING
+ * (GS_ERR_UNSUPPORTED for the fisheye kinds).  Uses the forward frame's
+ * projected buffer, values and tile_ranges (same surfels, sensor and opts;
+ * no overflow).  The backward recomposites every sample in fp32 from the
+ * Eq. 1 splat matrix and differentiates the front-to-back recurrence (two
+ * walks of each tile list).
+ *   grad_out   device [C,H,W] fp32 (C = 8 camera, 4 LiDAR)
+ *   workspace  device, >= gs_backward_workspace_bytes(n)
+ * Outputs (device, overwritten, zero for surfels that meet no sample):
+ *   d_means [n,3], d_quats [n,4] (w.r.t. the unnormalised input quaternion),
+ *   d_scales [n,2], d_opacities [n], camera: d_sh [n,(d+1)^2,3] (may be NULL);
+ *   LiDAR: d_intensity [n], d_raydrop_logit [n] (may be NULL).
+ * Per-surfel sums use fp32 atomics: results are not bitwise reproducible.
+ */
+size_t gs_backward_workspace_bytes(int64_t n);
+
+gs_status gs_render_backward(const gs_surfels *surfels, const gs_sensor *sensor, const gs_opts *opts,
+                             const void *projected, const uint32_t *values, const uint32_t *tile_ranges,
+                             const float *grad_out, void *workspace, size_t workspace_bytes, float *d_means,
+                             float *d_quats, float *d_scales, float *d_opacities, float *d_sh,
+                             float *d_intensity, float *d_raydrop_logit, gs_stream stream);
+
 const char *gs_status_string(gs_status status);
 const char *gs_last_error(void);
 

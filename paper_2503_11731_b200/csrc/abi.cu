@@ -26,6 +26,11 @@ cudaError_t launch_pack(const DevSurfels &s, int sh_floats, const uint32_t *inde
 cudaError_t launch_unpack(const float *in, int64_t m, int sh_floats, int has_int, int has_drop, float *means,
                           float *quats, float *scales, float *opac, float *sh, float *inten, float *drop,
                           cudaStream_t st);
+size_t backward_workspace_bytes(int64_t n);
+cudaError_t launch_backward(const DevSurfels &s, const DevSensor &se, const DevOpts &op, const void *proj,
+                            const uint32_t *values, const uint32_t *ranges, const float *gout, void *ws,
+                            float *d_means, float *d_quats, float *d_scales, float *d_opac, float *d_sh,
+                            float *d_int, float *d_drop, cudaStream_t st);
 cudaError_t launch_decode(const gs_anchors *, const gs_decoder *, const float[3], float *, float *, float *,
                           float *, float *, float *, float *, cudaStream_t);
 cudaError_t launch_render_camera(const void *, int64_t, const uint32_t *, const uint32_t *,
@@ -440,6 +445,41 @@ extern "C" gs_status gs_unpack_surfels(const float *payload, int64_t m, int32_t 
     const cudaError_t e = launch_unpack(payload, m, nsh, has_intensity != 0, has_raydrop != 0, means, quats, scales,
                                         opacities, sh, intensity, raydrop_logit, (cudaStream_t)stream);
     return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_unpack_surfels");
+}
+
+extern "C" size_t gs_backward_workspace_bytes(int64_t n) { return backward_workspace_bytes(n); }
+
+extern "C" gs_status gs_render_backward(const gs_surfels *sf, const gs_sensor *s, const gs_opts *o,
+                                        const void *projected, const uint32_t *values, const uint32_t *tile_ranges,
+                                        const float *grad_out, void *workspace, size_t workspace_bytes,
+                                        float *d_means, float *d_quats, float *d_scales, float *d_opacities,
+                                        float *d_sh, float *d_intensity, float *d_raydrop_logit, gs_stream stream) {
+    gs_status st;
+    if ((st = check_sensor(s)) != GS_OK) return st;
+    if ((st = check_opts(o)) != GS_OK) return st;
+    if ((st = check_tiles(s, o)) != GS_OK) return st;
+    if (s->kind != GS_PINHOLE && s->kind != GS_LIDAR_SPINNING)
+        return fail(GS_ERR_UNSUPPORTED, "gs_render_backward supports pinhole cameras and LiDAR");
+    if (!sf) return fail(GS_ERR_CONFIG, "surfels is NULL");
+    if (sf->n < 0) return fail(GS_ERR_CONFIG, "n < 0");
+    if (sf->n > 0 && (!sf->means || !sf->quats || !sf->scales || !sf->opacities || !projected || !values ||
+                      !tile_ranges || !grad_out || !workspace || !d_means || !d_quats || !d_scales || !d_opacities))
+        return fail(GS_ERR_CONFIG, "NULL buffer");
+    if (s->kind == GS_PINHOLE && sf->n > 0 && (!sf->sh || sf->sh_degree < 0 || sf->sh_degree > 3))
+        return fail(GS_ERR_CONFIG, "cameras need SH coefficients of degree 0..3");
+    if (workspace_bytes < backward_workspace_bytes(sf->n)) return fail(GS_ERR_CONFIG, "workspace too small");
+    DevSurfels ds;
+    ds.n = sf->n;
+    ds.means = sf->means; ds.quats = sf->quats; ds.scales = sf->scales; ds.opac = sf->opacities;
+    ds.sh = sf->sh; ds.inten = sf->intensity; ds.drop = sf->raydrop_logit;
+    ds.sh_degree = sf->sh_degree;
+    const DevSensor se = make_dev_sensor(s, o);
+    const DevOpts op = make_dev_opts(o);
+    const cudaError_t e = launch_backward(ds, se, op, projected, values, tile_ranges, grad_out, workspace, d_means,
+                                          d_quats, d_scales, d_opacities, d_sh, d_intensity, d_raydrop_logit,
+                                          (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gs_render_backward");
+    return GS_OK;
 }
 
 extern "C" const char *gs_status_string(gs_status s) {

@@ -69,7 +69,7 @@ class gs_decoder(C.Structure):
     _fields_ = [("modality", C.c_int32), ("head", gs_mlp * 6)]
 
 
-EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_band_route_workspace_bytes", "gs_band_route",
+EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_backward_workspace_bytes", "gs_render_backward", "gs_band_route_workspace_bytes", "gs_band_route",
            "gs_payload_floats", "gs_pack_surfels", "gs_unpack_surfels", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
            "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes",
@@ -133,6 +133,11 @@ def load(build_if_missing: bool = True):
     lib.gs_pack_surfels.restype = C.c_int
     lib.gs_unpack_surfels.argtypes = [vp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.gs_unpack_surfels.restype = C.c_int
+    lib.gs_backward_workspace_bytes.argtypes = [C.c_int64]
+    lib.gs_backward_workspace_bytes.restype = C.c_size_t
+    lib.gs_render_backward.argtypes = [P(gs_surfels), P(gs_sensor), P(gs_opts), vp, vp, vp, vp, vp, C.c_size_t,
+                                       vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.gs_render_backward.restype = C.c_int
     lib.gs_kernel_launches.argtypes = []
     lib.gs_kernel_launches.restype = C.c_uint64
     _lib = lib
@@ -291,6 +296,20 @@ def gs_unpack_surfels(payload, m, sh_degree, has_intensity, has_raydrop, means, 
                                     int(bool(has_raydrop)), _ptr(means), _ptr(quats), _ptr(scales),
                                     _ptr(opacities), _ptr(sh), _ptr(intensity), _ptr(raydrop_logit),
                                     C.c_void_p(stream)))
+
+
+def gs_backward_workspace_bytes(n):
+    return int(load().gs_backward_workspace_bytes(int(n)))
+
+
+def gs_render_backward(surfels: gs_surfels, sensor: Sensor, opts: gs_opts, projected, values, tile_ranges,
+                       grad_out, workspace, d_means, d_quats, d_scales, d_opacities, d_sh, d_intensity,
+                       d_raydrop_logit, stream):
+    _check(load().gs_render_backward(C.byref(surfels), sensor.ref, C.byref(opts), _ptr(projected), _ptr(values),
+                                     _ptr(tile_ranges), _ptr(grad_out), _ptr(workspace),
+                                     workspace.numel() * workspace.element_size(), _ptr(d_means), _ptr(d_quats),
+                                     _ptr(d_scales), _ptr(d_opacities), _ptr(d_sh), _ptr(d_intensity),
+                                     _ptr(d_raydrop_logit), C.c_void_p(stream)))
 
 
 def gs_kernel_launches() -> int:

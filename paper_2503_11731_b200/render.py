@@ -134,6 +134,25 @@ class Renderer:
                           ntiles=nt, sensor=sensor)
         return out
 
+    def backward(self, grad_out: torch.Tensor) -> dict:
+        """Gradients of sum(grad_out * out) for the last rendered frame w.r.t.
+        the surfel attributes (gs_render_backward; pinhole and LiDAR).
+        Returns {means, quats, scales, opacities, sh | intensity, raydrop_logit}."""
+        L = self._last
+        sensor = L["sensor"]
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        f = lambda t: None if t is None else torch.empty_like(t)
+        lidar = sensor.kind == gsr.GS_LIDAR_SPINNING
+        g = dict(means=f(self.t["means"]), quats=f(self.t["quats"]), scales=f(self.t["scales"]),
+                 opacities=f(self.t["opacities"]), sh=None if lidar else f(self.t.get("sh")),
+                 intensity=f(self.t.get("intensity")) if lidar else None,
+                 raydrop_logit=f(self.t.get("raydrop_logit")) if lidar else None)
+        ws = self._get("bwd_ws", gsr.gs_backward_workspace_bytes(self.n))
+        gsr.gs_render_backward(self.struct, sensor, self.opts, L["proj"], L["values"], L["ranges"],
+                               grad_out.contiguous(), ws, g["means"], g["quats"], g["scales"], g["opacities"],
+                               g["sh"], g["intensity"], g["raydrop_logit"], st)
+        return g
+
     def overflowed(self) -> bool:
         return bool(self._last["overflow"].item())
 
