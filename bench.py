@@ -165,9 +165,9 @@ def cpu_baseline(surfels, sensors, target_s=15.0, gpu_frames=None):
     r0, n0, t0 = oracle_rate(surfels, sensors, 64, 1234, cores, 1)   # calibration
     n = int(min(20000, max(64, r0 * target_s)))
     keep = []
-    r, n, t = oracle_rate(surfels, sensors, n, 4321, cores, keep=keep)
+    r, n, t = oracle_rate(surfels, sensors, n, 4321, cores, 8, keep=keep)
     cpu = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
-           "sample": f"{n} random rays over 4 random frames of the batch ({t:.1f} s of CPU work, "
+           "sample": f"{n} random rays over 8 random frames of the batch ({t:.1f} s of CPU work, "
                      f"fp64 brute force over all {surfels.n} surfels per ray, OpenMP {cores} threads)"}
     par = None
     if gpu_frames is not None:
@@ -605,7 +605,7 @@ def main():
     ap.add_argument("--gather", choices=["end", "rounds"], default="end",
                     help="N > 1: gather all frames after the batch (end) or one timestep round at a time as "
                          "soon as it is rendered, overlapping the transfer with rendering (rounds)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=24.0)
     ap.add_argument("--graph", action="store_true",
                     help="replay one CUDA graph of the whole local batch per step instead of enqueueing it "
                          "eagerly (measured A/B on the Chunked batch: 872 vs 882 Msamples/s -- the GPU, not "
