@@ -11,7 +11,10 @@
 // (opacity, colour | intensity, ray-drop) read [feature, view direction].
 //
 // One CTA = 128 anchors per tile (the M = 128 of a cta_group::1 tcgen05.mma),
-// persistent over tiles, 4 warps, 2 CTAs per SM.  The three layers are three
+// persistent over tiles, 8 warps (two per TMEM lane quarter: they split the
+// columns of every drain and the epilogue), 2 CTAs per SM; a tile's anchor
+// inputs are loaded one tile ahead and its outputs leave through shared
+// memory as coalesced 16-byte stores.  The three layers are three
 // chained GEMM groups with fp16 operands in shared memory (canonical K-major
 // no-swizzle UMMA layout) and fp32 accumulators in tensor memory:
 //   L1  [128 x 48] x [48 x 32H]      all heads at once (H = 5 camera, 6 LiDAR;
@@ -42,6 +45,7 @@ namespace gsr {
 namespace dec {
 
 constexpr int M = 128;                   // anchors per tile
+constexpr int NT = 2 * M;                // threads: two warps per TMEM lane quarter (columns split)
 constexpr int KS = GS_NEURAL_K;          // surfels per anchor
 constexpr int FEAT = GS_NEURAL_F;        // 32
 constexpr int HID = GS_NEURAL_HIDDEN;    // 32
@@ -62,6 +66,7 @@ constexpr int SZ_W2 = MAXH * HID * HID * 2;       // per head [32][32]
 constexpr int SZ_W3 = NOUT_PAD_MAX * HID * 2;     // [out rows][32]
 constexpr int SZ_A0 = M * K1 * 2;
 constexpr int SZ_A1 = M * MAXH * HID * 2;
+static_assert(13 * KS * M * 4 <= SZ_A1, "epilogue staging fits in A1");
 constexpr int OFF_W1 = 0;
 constexpr int OFF_W2 = OFF_W1 + SZ_W1;
 constexpr int OFF_W3 = OFF_W2 + SZ_W2;
@@ -168,32 +173,84 @@ __device__ __forceinline__ void tld16(uint32_t taddr, float *v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// (a0 + b0, a1 + b1) in one packed f32x2 add (sm_100), then ReLU and the
+// rounding to fp16 in one cvt: the same values as fmaxf(a + b, 0) -> fp16
+__device__ __forceinline__ uint32_t bias_relu_h2(float a0, float a1, float b0, float b1) {
+    uint32_t h;
+    asm("{\n\t.reg .b64 a, b, s;\n\t.reg .f32 lo, hi;\n\t"
+        "mov.b64 a, {%1, %2};\n\tmov.b64 b, {%3, %4};\n\t"
+        "add.rn.f32x2 s, a, b;\n\tmov.b64 {lo, hi}, s;\n\t"
+        "cvt.rn.relu.f16x2.f32 %0, hi, lo;\n\t}"
+        : "=r"(h) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+    return h;
+}
+
 // bias + ReLU + fp16 of 32 accumulator columns -> 4 K-chunks of row `row` of A
 __device__ __forceinline__ void relu_store(const float *v, const float *bias, char *A, int row, int k0, int kc) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float x0 = fmaxf(v[8 * c + 2 * q] + bias[8 * c + 2 * q], 0.f);
-            const float x1 = fmaxf(v[8 * c + 2 * q + 1] + bias[8 * c + 2 * q + 1], 0.f);
-            const __half2 h = __floats2half2_rn(x0, x1);
-            w[q] = *reinterpret_cast<const uint32_t *>(&h);
-        }
-        *reinterpret_cast<uint4 *>(A + cano(row, k0 + 8 * c, kc)) = make_uint4(w[0], w[1], w[2], w[3]);
+        const float4 b0 = *reinterpret_cast<const float4 *>(bias + 8 * c);
+        const float4 b1 = *reinterpret_cast<const float4 *>(bias + 8 * c + 4);
+        const float *x = v + 8 * c;
+        *reinterpret_cast<uint4 *>(A + cano(row, k0 + 8 * c, kc)) =
+            make_uint4(bias_relu_h2(x[0], x[1], b0.x, b0.y), bias_relu_h2(x[2], x[3], b0.z, b0.w),
+                       bias_relu_h2(x[4], x[5], b1.x, b1.y), bias_relu_h2(x[6], x[7], b1.z, b1.w));
     }
 }
 
-__device__ __forceinline__ float sigm(float z) { return 1.f / (1.f + __expf(-z)); }
+// Gram-Schmidt frame of surfel j's 6D rotation output (a1, a2) and its
+// quaternion (w >= 0) by Shepperd's method on the largest of 1+tr, 1+2R_ii-tr
+__device__ __forceinline__ void write_quat(const float *R, const float *B3, int j, float *q) {
+    float a1x = R[6 * j] + B3[32 + 6 * j], a1y = R[6 * j + 1] + B3[32 + 6 * j + 1], a1z = R[6 * j + 2] + B3[32 + 6 * j + 2];
+    float a2x = R[6 * j + 3] + B3[32 + 6 * j + 3], a2y = R[6 * j + 4] + B3[32 + 6 * j + 4],
+          a2z = R[6 * j + 5] + B3[32 + 6 * j + 5];
+    const float i1 = rsqrtf(a1x * a1x + a1y * a1y + a1z * a1z);
+    const float ux = a1x * i1, uy = a1y * i1, uz = a1z * i1;
+    const float dp = ux * a2x + uy * a2y + uz * a2z;
+    a2x -= dp * ux; a2y -= dp * uy; a2z -= dp * uz;
+    const float i2 = rsqrtf(a2x * a2x + a2y * a2y + a2z * a2z);
+    const float vx = a2x * i2, vy = a2y * i2, vz = a2z * i2;
+    const float nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+    const float tr = ux + vy + nz;
+    float qw, qx, qy, qz;
+    if (tr >= fmaxf(ux, fmaxf(vy, nz))) {
+        const float h = sqrtf(fmaxf(1.f + tr, 0.f)), ir = __fdividef(0.5f, h);   // r4 = 2h
+        qw = 0.5f * h; qx = (vz - ny) * ir; qy = (nx - uz) * ir; qz = (uy - vx) * ir;
+    } else if (ux >= vy && ux >= nz) {
+        const float h = sqrtf(fmaxf(1.f + ux - vy - nz, 0.f)), ir = __fdividef(0.5f, h);
+        qw = (vz - ny) * ir; qx = 0.5f * h; qy = (vx + uy) * ir; qz = (nx + uz) * ir;
+    } else if (vy >= nz) {
+        const float h = sqrtf(fmaxf(1.f - ux + vy - nz, 0.f)), ir = __fdividef(0.5f, h);
+        qw = (nx - uz) * ir; qx = (vx + uy) * ir; qy = 0.5f * h; qz = (ny + vz) * ir;
+    } else {
+        const float h = sqrtf(fmaxf(1.f - ux - vy + nz, 0.f)), ir = __fdividef(0.5f, h);
+        qw = (uy - vx) * ir; qx = (nx + uz) * ir; qy = (ny + vz) * ir; qz = 0.5f * h;
+    }
+    if (qw < 0.f) { qw = -qw; qx = -qx; qy = -qy; qz = -qz; }
+    *reinterpret_cast<float4 *>(q) = make_float4(qw, qx, qy, qz);
+}
+
+// staged tile outputs -> global, 16-byte stores (dst 16-byte aligned: every
+// array's tile slice starts at a multiple of 4 floats)
+__device__ __forceinline__ void copy_out(const float *src, float *dst, int nfl, int t) {
+    const int n4 = nfl >> 2;
+    for (int i = t; i < n4; i += NT)
+        reinterpret_cast<float4 *>(dst)[i] = reinterpret_cast<const float4 *>(src)[i];
+    for (int i = 4 * n4 + t; i < nfl; i += NT) dst[i] = src[i];
+}
+
+__device__ __forceinline__ float sigm(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
 
 template <int LIDAR>
-__global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NT, 2) k_decode(const __grid_constant__ Params p) {
     constexpr int H = LIDAR ? 6 : 5;
     constexpr int N1 = H * HID;
     constexpr int KC1 = K1 / 8, KC2 = N1 / 8;
     extern __shared__ __align__(1024) char sm[];
     __shared__ uint32_t s_tmem;
     const int t = threadIdx.x, warp = t >> 5;
+    const int row = t & (M - 1);   // anchor row of the tile = TMEM lane
+    const int grp = t >> 7;        // 0: warps 0-3, 1: warps 4-7 (same lane quarters, other columns)
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     char *W1 = sm + OFF_W1, *W2 = sm + OFF_W2, *W3 = sm + OFF_W3, *A0 = sm + OFF_A0, *A1 = sm + OFF_A1;
     float *B1 = reinterpret_cast<float *>(sm + OFF_B1), *B2 = reinterpret_cast<float *>(sm + OFF_B2),
@@ -209,17 +266,17 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
         bar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    for (int e = t; e < N1 * K1; e += M) {   // L1: row r = 32h + i, K = [feature | view | 0]
+    for (int e = t; e < N1 * K1; e += NT) {   // L1: row r = 32h + i, K = [feature | view | 0]
         const int r = e / K1, k = e % K1, h = r / HID, i = r % HID;
         const int nin = h < 3 ? FEAT : FEAT + 3;
         const __half w = k < nin ? p.w1[h][i * nin + k] : __float2half(0.f);
         *reinterpret_cast<__half *>(W1 + cano(r, k, KC1)) = w;
     }
-    for (int e = t; e < H * HID * HID; e += M) {   // L2: per head [32][32]
+    for (int e = t; e < H * HID * HID; e += NT) {   // L2: per head [32][32]
         const int h = e / (HID * HID), r = (e / HID) % HID, k = e % HID;
         *reinterpret_cast<__half *>(W2 + h * HID * HID * 2 + cano(r, k, HID / 8)) = p.w2[h][r * HID + k];
     }
-    for (int e = t; e < NOUT_PAD_MAX * HID; e += M) {   // L3: rows OUT_COL[h] + i, zero-padded
+    for (int e = t; e < NOUT_PAD_MAX * HID; e += NT) {   // L3: rows OUT_COL[h] + i, zero-padded
         const int r = e / HID, k = e % HID;
         __half w = __float2half(0.f);
         float b = 0.f;
@@ -234,7 +291,7 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
         *reinterpret_cast<__half *>(W3 + cano(r, k, HID / 8)) = w;
         if (k == 0) B3[r] = b;
     }
-    for (int e = t; e < N1; e += M) {
+    for (int e = t; e < N1; e += NT) {
         B1[e] = p.b1[e / HID][e % HID];
         B2[e] = p.b2[e / HID][e % HID];
     }
@@ -243,35 +300,49 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
     __syncthreads();
     tc_after();
     const uint32_t tmem = s_tmem;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);   // this warp's lane quarter
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's lane quarter
     uint32_t phase = 0;
 
     const int64_t ntiles = (p.n + M - 1) / M;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t a = tile * M + t;
-        const bool live = a < p.n;
-        // ---- anchor row -> A0 (features, fp16 view direction, zero pad)
-        float x = 0.f, y = 0.f, z = 0.f;
-        uint4 f4[4] = {};
-        if (live) {
-            x = __ldg(p.pos + 3 * a);
-            y = __ldg(p.pos + 3 * a + 1);
-            z = __ldg(p.pos + 3 * a + 2);
-            const uint4 *fp = reinterpret_cast<const uint4 *>(p.feat) + 4 * a;
+    // the anchor inputs of a tile are loaded one tile ahead (they arrive while the
+    // previous tile's MMAs, drains and epilogue run): group 0 the position and base
+    // scale, group 1 the feature
+    float nx_ = 0.f, ny_ = 0.f, nz_ = 0.f, nl0 = 0.f, nl1 = 0.f, nl2 = 0.f;
+    uint4 nf[4] = {};
+    auto prefetch = [&](int64_t tl) {
+        const int64_t an = tl * M + row;
+        if (tl >= ntiles || an >= p.n) return;
+        if (grp == 0) {
+            nx_ = __ldg(p.pos + 3 * an); ny_ = __ldg(p.pos + 3 * an + 1); nz_ = __ldg(p.pos + 3 * an + 2);
+            nl0 = __ldg(p.base + 3 * an); nl1 = __ldg(p.base + 3 * an + 1); nl2 = __ldg(p.base + 3 * an + 2);
+        } else {
+            const uint4 *fp = reinterpret_cast<const uint4 *>(p.feat) + 4 * an;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) f4[c] = __ldg(fp + c);
+            for (int c = 0; c < 4; ++c) nf[c] = __ldg(fp + c);
         }
-        {
+    };
+    prefetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t a = tile * M + row;
+        const bool live = a < p.n;
+        // ---- anchor row -> A0 (features, fp16 view direction, zero pad): group 0 the
+        // view direction, group 1 the feature chunks
+        const float x = live ? nx_ : 0.f, y = live ? ny_ : 0.f, z = live ? nz_ : 0.f;
+        const float l0 = nl0, l1 = nl1, l2 = nl2;
+        if (grp == 0) {
             const float vx = x - p.ox, vy = y - p.oy, vz = z - p.oz;
-            const float inv = live ? 1.f / sqrtf(vx * vx + vy * vy + vz * vz) : 0.f;
+            const float inv = live ? rsqrtf(vx * vx + vy * vy + vz * vz) : 0.f;
             const __half2 d01 = __floats2half2_rn(vx * inv, vy * inv);
             const __half2 d2z = __floats2half2_rn(vz * inv, 0.f);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) *reinterpret_cast<uint4 *>(A0 + cano(t, 8 * c, KC1)) = f4[c];
-            *reinterpret_cast<uint4 *>(A0 + cano(t, 32, KC1)) =
+            *reinterpret_cast<uint4 *>(A0 + cano(row, 32, KC1)) =
                 make_uint4(*reinterpret_cast<const uint32_t *>(&d01), *reinterpret_cast<const uint32_t *>(&d2z), 0u, 0u);
-            *reinterpret_cast<uint4 *>(A0 + cano(t, 40, KC1)) = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4 *>(A0 + cano(row, 40, KC1)) = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<uint4 *>(A0 + cano(row, 8 * c, KC1)) = live ? nf[c] : make_uint4(0u, 0u, 0u, 0u);
         }
+        prefetch(tile + gridDim.x);
         // ---- L1: [128 x 48] x [48 x 32H]
         fence_async_smem();
         tc_before();
@@ -287,12 +358,12 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
         bar_wait(bar, phase);
         phase ^= 1;
         tc_after();
-        {
+        {   // heads 0-2 by group 0, 3.. by group 1
             float v[32];
 #pragma unroll 1
-            for (int h = 0; h < H; ++h) {
+            for (int h = grp * 3; h < (grp ? H : 3); ++h) {
                 tld32(trow + 32 * h, v);
-                relu_store(v, B1 + 32 * h, A1, t, 32 * h, KC2);
+                relu_store(v, B1 + 32 * h, A1, row, 32 * h, KC2);
             }
         }
         // ---- L2: per head [128 x 32] x [32 x 32]
@@ -312,12 +383,12 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
         bar_wait(bar, phase);
         phase ^= 1;
         tc_after();
-        {
+        {   // heads 0-2 by group 0, 3.. by group 1
             float v[32];
 #pragma unroll 1
-            for (int h = 0; h < H; ++h) {
+            for (int h = grp * 3; h < (grp ? H : 3); ++h) {
                 tld32(trow + 32 * h, v);
-                relu_store(v, B2 + 32 * h, A1, t, 32 * h, KC2);
+                relu_store(v, B2 + 32 * h, A1, row, 32 * h, KC2);
             }
         }
         // ---- L3: per head [128 x 32] x [32 x out_pad]
@@ -338,65 +409,67 @@ __global__ void __launch_bounds__(M, 2) k_decode(const __grid_constant__ Params 
         bar_wait(bar, phase);
         phase ^= 1;
         tc_after();
-        // ---- epilogue: 5 surfels of this anchor
-        float O[16], S[16], R[32], Op[16], C[16], D[16];
-        tld16(trow + 0, O);
-        tld16(trow + 16, S);
+        // ---- epilogue: 5 surfels of this anchor, split between the two groups
+        // (group 0: centres, scales, frames of surfels 0-2; group 1: frames of
+        // surfels 3-4, opacity, colour | intensity and ray-drop), staged in A1
+        // (free until the next tile's L1 drain) and then stored coalesced
+        float *stg = reinterpret_cast<float *>(A1);
+        float *sM = stg, *sQ = sM + 3 * KS * M, *sS = sQ + 4 * KS * M, *sO = sS + 2 * KS * M;
+        float *sC = sO + KS * M;   // camera: 3 per surfel; LiDAR: intensity, then ray-drop logit
+        const int ls0 = KS * row;  // this anchor's first surfel in the tile
+        float R[32];
         tld32(trow + 32, R);
-        tld16(trow + 64, Op);
-        tld16(trow + 80, C);
-        if (LIDAR) tld16(trow + 96, D);
-        tc_before();   // the next tile's L1 overwrites these columns after the CTA barrier
-        if (live) {
-            const float l0 = __ldg(p.base + 3 * a), l1 = __ldg(p.base + 3 * a + 1), l2 = __ldg(p.base + 3 * a + 2);
+        if (grp == 0) {
+            float O[16], S[16];
+            tld16(trow + 0, O);
+            tld16(trow + 16, S);
+            tc_before();   // the next tile's L1 overwrites these columns after the CTA barrier
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
-                const int64_t s = (int64_t)KS * a + j;
-                float *mu = p.means + 3 * s;
-                mu[0] = fmaf(O[3 * j] + B3[3 * j], l0, x);
-                mu[1] = fmaf(O[3 * j + 1] + B3[3 * j + 1], l1, y);
-                mu[2] = fmaf(O[3 * j + 2] + B3[3 * j + 2], l2, z);
-                p.scales[2 * s] = l0 * expf(S[2 * j] + B3[16 + 2 * j]);
-                p.scales[2 * s + 1] = l1 * expf(S[2 * j + 1] + B3[16 + 2 * j + 1]);
-                // Gram-Schmidt frame of the 6D output, then its quaternion (w >= 0)
-                float a1x = R[6 * j] + B3[32 + 6 * j], a1y = R[6 * j + 1] + B3[32 + 6 * j + 1],
-                      a1z = R[6 * j + 2] + B3[32 + 6 * j + 2];
-                float a2x = R[6 * j + 3] + B3[32 + 6 * j + 3], a2y = R[6 * j + 4] + B3[32 + 6 * j + 4],
-                      a2z = R[6 * j + 5] + B3[32 + 6 * j + 5];
-                const float i1 = 1.f / sqrtf(a1x * a1x + a1y * a1y + a1z * a1z);
-                const float ux = a1x * i1, uy = a1y * i1, uz = a1z * i1;
-                const float dp = ux * a2x + uy * a2y + uz * a2z;
-                a2x -= dp * ux; a2y -= dp * uy; a2z -= dp * uz;
-                const float i2 = 1.f / sqrtf(a2x * a2x + a2y * a2y + a2z * a2z);
-                const float vx = a2x * i2, vy = a2y * i2, vz = a2z * i2;
-                const float nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
-                // R = [u v n] (columns); Shepperd's method on the largest of 1+tr, 1+2R_ii-tr
-                const float tr = ux + vy + nz;
-                float qw, qx, qy, qz;
-                if (tr >= fmaxf(ux, fmaxf(vy, nz))) {
-                    const float r4 = 2.f * sqrtf(fmaxf(1.f + tr, 0.f));
-                    qw = 0.25f * r4; qx = (vz - ny) / r4; qy = (nx - uz) / r4; qz = (uy - vx) / r4;
-                } else if (ux >= vy && ux >= nz) {
-                    const float r4 = 2.f * sqrtf(fmaxf(1.f + ux - vy - nz, 0.f));
-                    qw = (vz - ny) / r4; qx = 0.25f * r4; qy = (vx + uy) / r4; qz = (nx + uz) / r4;
-                } else if (vy >= nz) {
-                    const float r4 = 2.f * sqrtf(fmaxf(1.f - ux + vy - nz, 0.f));
-                    qw = (nx - uz) / r4; qx = (vx + uy) / r4; qy = 0.25f * r4; qz = (ny + vz) / r4;
-                } else {
-                    const float r4 = 2.f * sqrtf(fmaxf(1.f - ux - vy + nz, 0.f));
-                    qw = (uy - vx) / r4; qx = (nx + uz) / r4; qy = (ny + vz) / r4; qz = 0.25f * r4;
-                }
-                if (qw < 0.f) { qw = -qw; qx = -qx; qy = -qy; qz = -qz; }
-                *reinterpret_cast<float4 *>(p.quats + 4 * s) = make_float4(qw, qx, qy, qz);
-                p.opac[s] = sigm(Op[j] + B3[64 + j]);
-                if (!LIDAR) {
-                    const float C0 = 0.28209479177387814f;
+                const int ls = ls0 + j;
+                sM[3 * ls] = fmaf(O[3 * j] + B3[3 * j], l0, x);
+                sM[3 * ls + 1] = fmaf(O[3 * j + 1] + B3[3 * j + 1], l1, y);
+                sM[3 * ls + 2] = fmaf(O[3 * j + 2] + B3[3 * j + 2], l2, z);
+                *reinterpret_cast<float2 *>(sS + 2 * ls) =
+                    make_float2(l0 * __expf(S[2 * j] + B3[16 + 2 * j]), l1 * __expf(S[2 * j + 1] + B3[16 + 2 * j + 1]));
+            }
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) p.sh[3 * s + c] = (sigm(C[3 * j + c] + B3[80 + 3 * j + c]) - 0.5f) / C0;
+            for (int j = 0; j < 3; ++j) write_quat(R, B3, j, sQ + 4 * (ls0 + j));
+        } else {
+            float Op[16], C[16], D[16];
+            tld16(trow + 64, Op);
+            tld16(trow + 80, C);
+            if (LIDAR) tld16(trow + 96, D);
+            tc_before();
+#pragma unroll
+            for (int j = 3; j < KS; ++j) write_quat(R, B3, j, sQ + 4 * (ls0 + j));
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                const int ls = ls0 + j;
+                sO[ls] = sigm(Op[j] + B3[64 + j]);
+                if (!LIDAR) {
+                    const float iC0 = 3.5449077018110318f;   // 1 / C0 = 2 sqrt(pi)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) sC[3 * ls + c] = (sigm(C[3 * j + c] + B3[80 + 3 * j + c]) - 0.5f) * iC0;
                 } else {
-                    p.inten[s] = sigm(C[j] + B3[80 + j]);
-                    p.drop[s] = D[j] + B3[96 + j];
+                    sC[ls] = sigm(C[j] + B3[80 + j]);
+                    sC[KS * M + ls] = D[j] + B3[96 + j];
                 }
+            }
+        }
+        __syncthreads();
+        {
+            const int64_t s0 = (int64_t)KS * tile * M;                       // first surfel of the tile
+            const int ns = (int)min((int64_t)KS * M, (int64_t)KS * p.n - s0);   // its live surfels
+            copy_out(sM, p.means + 3 * s0, 3 * ns, t);
+            copy_out(sQ, p.quats + 4 * s0, 4 * ns, t);
+            copy_out(sS, p.scales + 2 * s0, 2 * ns, t);
+            copy_out(sO, p.opac + s0, ns, t);
+            if (!LIDAR) {
+                copy_out(sC, p.sh + 3 * s0, 3 * ns, t);
+            } else {
+                copy_out(sC, p.inten + s0, ns, t);
+                copy_out(sC + KS * M, p.drop + s0, ns, t);
             }
         }
     }
@@ -441,11 +514,11 @@ cudaError_t launch_decode(const gs_anchors *an, const gs_decoder *de, const floa
     int dev = 0, nsm = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, M, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, SMEM);
     const int64_t ntiles = (p.n + M - 1) / M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)nsm * std::max(1, std::min(per, 2)));
     note_launch();
-    kern<<<grid, M, SMEM, st>>>(p);
+    kern<<<grid, NT, SMEM, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,7 @@
+python paper_2503_11731_b200/build.py > gpurun_out/r2f_build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r2f_gputest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/r2f_gputest.log
+timeout 300 python tools/sweep.py fisheye 16x8 > gpurun_out/r2f_sweep.jsonl 2>&1
+timeout 300 python tools/sweep.py lidar 16x8 32x1 0 0,2048,4096,8192 >> gpurun_out/r2f_sweep.jsonl 2>&1
+timeout 600 python tools/sweep.py chunked 16x8,16x16 32x1 0 0,4096 >> gpurun_out/r2f_sweep.jsonl 2>&1
+grep frame gpurun_out/r2f_sweep.jsonl
