@@ -129,13 +129,18 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
     if (d_overflow && *d_overflow) return;
     const uint32_t n = *d_n;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t mask = (1u << bits) - 1;
+    const uint32_t lt = lanemask_lt();
+    // persistent: the CTA takes tiles in order from the dynamic counter until the
+    // keys are exhausted (the element count is only known on the device, so a grid
+    // sized for the capacity would otherwise launch waves of empty CTAs)
+    while (true) {
     if (tid == 0) s_tile = atomicAdd(counter, 1u);
     for (int i = tid; i < RS_WARPS * RS_BINS; i += RS_THREADS) (&whist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t t0 = tile * RS_TILE;
     if (t0 >= n) return;
-    const uint32_t mask = (1u << bits) - 1;
     const uint32_t wbase = t0 + warp * (32 * RS_ITEMS);
     uint32_t k[RS_ITEMS], v[RS_ITEMS], rk[RS_ITEMS];
 #pragma unroll
@@ -151,7 +156,6 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
     // reservation precedes item j+1's) and broadcasts the old count.  The 16
     // matches and atomics are independent, so they overlap instead of forming a
     // load/store chain through shared memory.
-    const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         const uint32_t idx = wbase + j * 32 + lane;
@@ -235,6 +239,8 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
         kout[dst] = key;
         vout[dst] = sval[i];
     }
+    __syncthreads();   // shared memory is reused by the next tile
+    }
 }
 
 // ------------------------------------------------------------------ pair offsets
@@ -288,67 +294,98 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_pair_offsets(
 }
 
 // ------------------------------------------------------------------ emission
-// Warp-cooperative: a warp takes 32 consecutive visible surfels (depth
-// order), whose pairs occupy one contiguous output range; lane q of each
-// round writes pair q of that range (coalesced), locating its surfel by a
-// binary search over the warp's exclusive pair counts.  Pairs of a surfel
-// are its tiles row-major (tile column modulo ntx: LiDAR azimuth wrap).
-// The per-digit histograms of the tile sort (npass x 8-bit digits) are
-// accumulated on the way in shared memory and added to `thist`.
+// Load-balanced by pairs: warp task c emits pairs [c*EM_CH, (c+1)*EM_CH) of
+// the depth-ordered pair list (coalesced), whatever the surfels' sizes (a
+// few near surfels covering thousands of tiles no longer serialise one
+// warp).  The task's first surfel is found by a 32-ary warp search of the
+// emission offsets; then the warp takes the surfels from there in groups of
+// 32: lane q of each round writes one pair, locating its surfel by a binary
+// search over the group's offsets (shuffles).  Pairs of a surfel are its
+// tiles row-major (tile column modulo ntx: LiDAR azimuth wrap).  The
+// per-digit histograms of the tile sort (npass x 8-bit digits) are
+// accumulated in shared memory and added to `thist`.
+constexpr uint32_t EM_CH = 1024;   // pairs per warp task
+
+__device__ __forceinline__ uint32_t first_surfel(const uint32_t *__restrict__ offs, uint32_t n, uint32_t q0,
+                                                 int lane) {
+    // largest k < n with offs[k] <= q0 (offs ascending, offs[0] = 0 <= q0)
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) >> 5;
+        const uint32_t idx = lo + (uint32_t)lane * step;
+        const bool le = idx < hi && __ldg(offs + idx) <= q0;
+        const uint32_t b = __ballot_sync(FULL_MASK, le);
+        const uint32_t last = 31 - __clz(b);   // lane 0 probes lo: always set
+        lo += last * step;
+        hi = min(hi, lo + step);
+    }
+    const uint32_t idx = lo + (uint32_t)lane;
+    const bool le = idx < hi && __ldg(offs + idx) <= q0;
+    return lo + 31 - __clz(__ballot_sync(FULL_MASK, le));
+}
+
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
                                               const uint32_t *__restrict__ offs,
                                               const short4 *__restrict__ rect,
-                                              const ProjHeader *hdr, int ntx, int npass, int tbits,
-                                              uint32_t *__restrict__ tkey,
+                                              const ProjHeader *hdr, const uint32_t *d_np, int ntx, int npass,
+                                              int tbits, uint32_t *__restrict__ tkey,
                                               uint32_t *__restrict__ tval, uint32_t *__restrict__ thist,
                                               const int32_t *d_overflow) {
     __shared__ uint32_t h[3][RS_BINS];
     if (*d_overflow) return;
     for (int i = threadIdx.x; i < 3 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
-    const uint32_t n = hdr->n_visible;
+    const uint32_t n = hdr->n_visible, P = *d_np;
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < n; w += nwarps) {
-        const uint32_t k = w * 32 + lane;
-        uint32_t id = 0, c = 0, o0 = 0;
-        int x0 = 0, y0 = 0, wd = 1;
-        if (k < n) {
-            id = sid[k];
-            const short4 r = rect[id];
-            x0 = r.x; y0 = r.y;
-            wd = r.z - r.x + 1;
-            c = (uint32_t)(wd * (r.w - r.y + 1));
-            o0 = offs[k];
-        }
-        const uint32_t base = __shfl_sync(FULL_MASK, o0, 0);
-        const uint32_t inc = warp_inclusive_scan<uint32_t>(c);
-        const uint32_t lo = inc - c;
-        const uint32_t total = __shfl_sync(FULL_MASK, inc, 31);
-        for (uint32_t o = 0; o < total; o += 32) {
-            const uint32_t q = o + lane;
-            int idx = 0;
-#pragma unroll
-            for (int step = 16; step; step >>= 1) {
-                const uint32_t l = __shfl_sync(FULL_MASK, lo, idx + step);
-                if (q >= l && idx + step < 32) idx += step;
+    const uint32_t ntask = (P + EM_CH - 1) / EM_CH;
+    for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ntask; c += nwarps) {
+        const uint32_t q0 = c * EM_CH, q1 = min(P, q0 + EM_CH);
+        uint32_t k = first_surfel(offs, n, q0, lane);
+        while (true) {
+            // the group of surfels k .. k+31 and their pair offsets
+            const uint32_t kk = k + (uint32_t)lane;
+            uint32_t id = 0, o0 = 0xffffffffu;
+            int x0 = 0, y0 = 0, wd = 1;
+            if (kk < n) {
+                id = sid[kk];
+                const short4 r = rect[id];
+                x0 = r.x; y0 = r.y;
+                wd = r.z - r.x + 1;
+                o0 = offs[kk];
             }
-            const uint32_t rid = __shfl_sync(FULL_MASK, id, idx);
-            const uint32_t rlo = __shfl_sync(FULL_MASK, lo, idx);
-            const int rx0 = __shfl_sync(FULL_MASK, x0, idx), ry0 = __shfl_sync(FULL_MASK, y0, idx);
-            const int rw = __shfl_sync(FULL_MASK, wd, idx);
-            if (q < total) {
-                const uint32_t r = q - rlo;
-                const int dy = (int)(r / (uint32_t)rw), dx = (int)(r - (uint32_t)dy * (uint32_t)rw);
-                const int tx = rx0 + dx;
-                const uint32_t tile = (uint32_t)((ry0 + dy) * ntx + (tx >= ntx ? tx - ntx : tx));
-                tkey[base + q] = tile;
-                tval[base + q] = rid;
-                for (int p = 0; p < npass; ++p) {
-                    const int bits = min(8, tbits - 8 * p);
-                    atomicAdd(&h[p][(tile >> (8 * p)) & ((1u << bits) - 1)], 1u);
+            const uint32_t gbeg = max(q0, __shfl_sync(FULL_MASK, o0, 0));
+            // end of the group's pairs: offset of surfel k+32 (or P), clipped to the task
+            const uint32_t onext = k + 32 < n ? __ldg(offs + k + 32) : P;
+            const uint32_t gend = min(q1, onext);
+            for (uint32_t qb = gbeg; qb < gend; qb += 32) {
+                const uint32_t q = qb + (uint32_t)lane;
+                // last lane of the group whose first pair is <= q (o0 ascending; unused lanes hold ~0)
+                int idx = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const uint32_t l = __shfl_sync(FULL_MASK, o0, idx + step);
+                    if (idx + step < 32 && l <= q) idx += step;
+                }
+                const uint32_t rid = __shfl_sync(FULL_MASK, id, idx);
+                const uint32_t rlo = __shfl_sync(FULL_MASK, o0, idx);
+                const int rx0 = __shfl_sync(FULL_MASK, x0, idx), ry0 = __shfl_sync(FULL_MASK, y0, idx);
+                const int rw = __shfl_sync(FULL_MASK, wd, idx);
+                if (q < gend) {
+                    const uint32_t r = q - rlo;
+                    const int dy = (int)(r / (uint32_t)rw), dx = (int)(r - (uint32_t)dy * (uint32_t)rw);
+                    const int tx = rx0 + dx;
+                    const uint32_t tile = (uint32_t)((ry0 + dy) * ntx + (tx >= ntx ? tx - ntx : tx));
+                    tkey[q] = tile;
+                    tval[q] = rid;
+                    for (int p = 0; p < npass; ++p) {
+                        const int bits = min(8, tbits - 8 * p);
+                        atomicAdd(&h[p][(tile >> (8 * p)) & ((1u << bits) - 1)], 1u);
+                    }
                 }
             }
+            if (onext >= q1 || k + 32 >= n) break;
+            k += 32;
         }
     }
     __syncthreads();
@@ -448,7 +485,12 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     note_launch();
     k_hist_scan<<<1, RS_BINS, 0, st>>>(hist, 4, nullptr);
     CK(cudaGetLastError());
-    const unsigned grid_d = (unsigned)(W.ntile_d > 0 ? W.ntile_d : 1);
+    int dev = 0, nsm = 148, per_os = 3;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_os, k_onesweep, RS_THREADS, 0);
+    const int64_t resident = (int64_t)nsm * std::max(per_os, 1);   // persistent onesweep CTAs
+    const unsigned grid_d = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)W.ntile_d, resident));
     for (int p = 0; p < 4; ++p) {
         note_launch();
         k_onesweep<<<grid_d, RS_THREADS, 0, st>>>(ki, vi, bufk[p & 1], bufv[p & 1], d_nvis, 8 * p, 8,
@@ -478,18 +520,17 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     const int tb = tile_bits_for(ntiles);
     const uint32_t *d_np = &misc->n_pairs32;
     uint32_t *thist = hist + 4 * RS_BINS;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)nsm * 8));
-    k_emit<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr, ntx, np, tb, tk[cur], tv[cur],
+    // P is only known on the device: enough warps for the capacity's tasks, at most 8 CTAs per SM
+    const int64_t tasks = (cap + EM_CH - 1) / EM_CH;
+    const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, (int64_t)nsm * 8));
+    k_emit<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr, d_np, ntx, np, tb, tk[cur], tv[cur],
                                thist, d_overflow);
     CK(cudaGetLastError());
     // 3. tile digits over the pairs
     note_launch();
     k_hist_scan<<<1, RS_BINS, 0, st>>>(thist, np, d_overflow);
     CK(cudaGetLastError());
-    const unsigned grid_t = (unsigned)(W.ntile_t > 0 ? W.ntile_t : 1);
+    const unsigned grid_t = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)W.ntile_t, resident));
     for (int p = 0; p < np; ++p) {
         const int bits = min(8, tb - 8 * p);
         note_launch();
