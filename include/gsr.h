@@ -157,8 +157,14 @@ int64_t gs_num_tiles(const gs_sensor *sensor, const gs_opts *opts);
  * sensor-frame local-to-sensor map of Eq. 1 in its intersection form, the
  * projected centre, the fp32 depth key (DESIGN reading R9), the oriented
  * normal, the SH colour (cameras) or intensity / ray-drop probability
- * (LiDAR), and a conservative 3-sigma bound as a rectangle of tiles.
- * Then compacts the visible surfels and counts the (tile, surfel) pairs.
+ * (LiDAR), and the exact set of tiles whose samples the surfel's 3-sigma
+ * support (cameras: or its low-pass disc) can reach: pinhole, per tile row
+ * the columns the support conic / disc meets (widened by a slack above the
+ * compositor's fp32 error); LiDAR (one-row tiles), per tile a conservative
+ * minimum of the support quadric over the tile's ray arc; fisheye, the
+ * conservative 3-sigma rectangle of tiles.  The stored rect is the hull of
+ * the set.  Then compacts the visible surfels and counts the (tile, surfel)
+ * pairs (the sizes of those sets).
  *   projected       device buffer of >= gs_projected_bytes(n, kind) bytes (out)
  *   d_num_pairs     device int64 (out): total number of pairs P
  */
@@ -174,7 +180,10 @@ gs_status gs_project(const gs_surfels *surfels, const gs_sensor *sensor, const g
  * (tile << 32 | depth-key bits) pair keys (ties by surfel index), then tile
  * ranges.  The 32 depth bits are sorted once per visible surfel before the
  * pairs are emitted (an LSD sort may do its low digits on any order-preserving
- * expansion); the tile digits are then sorted over the P pairs.
+ * expansion); the tile digits are then sorted over the P pairs.  A surfel's
+ * pairs are the tile set gs_project counted (pinhole: the same row
+ * intervals, recomputed from the same record floats; LiDAR: the stored tile
+ * mask).
  *   projected       buffer written by gs_project for the same surfels/sensor/opts
  *   keys            device [pair_capacity] u64 (out, may be NULL): sorted keys
  *   values          device [pair_capacity] u32 (out): surfel index of each sorted pair

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libgsr.so")
 SOURCES = ["abi.cu", "project.cu", "sort.cu", "render.cu", "decode.cu", "route.cu", "backward.cu"]
-HEADERS = ["gsr_internal.cuh", "scan.cuh"]
+HEADERS = ["gsr_internal.cuh", "scan.cuh", "binning.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]

@@ -13,7 +13,7 @@ namespace gsr {
 cudaError_t launch_project(const DevSurfels &, const DevSensor &, const DevOpts &, void *, int64_t *,
                            cudaStream_t);
 size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles);
-cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
+cudaError_t launch_bin_sort(const void *proj, int64_t n, const DevSensor &se, int64_t ntiles,
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges, void *ws,
                             int32_t *d_overflow, cudaStream_t st);
 size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix);
@@ -294,8 +294,8 @@ extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sens
     const int64_t nt = gs_num_tiles(s, o);
     if (nt >= (1ll << 24)) return fail(GS_ERR_RANGE, "too many tiles");
     if (workspace_bytes < sort_workspace_bytes(n, cap, nt)) return fail(GS_ERR_CONFIG, "workspace too small");
-    const int ntx = (s->width + o->tile_w - 1) / o->tile_w;
-    cudaError_t e = launch_bin_sort(projected, n, s->kind, ntx, nt, keys, values, cap, tile_ranges, workspace,
+    const DevSensor se = make_dev_sensor(s, o);
+    cudaError_t e = launch_bin_sort(projected, n, se, nt, keys, values, cap, tile_ranges, workspace,
                                     d_overflow, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_bin_sort");
     return GS_OK;

@@ -93,7 +93,14 @@ __host__ __device__ inline int record_floats(int kind) {
 
 // ---------------------------------------------------------------- projected buffer
 // [ header 256 B | records n*rec | rect n*8 | key n*4 | count n*4 |
-//   vis_key n*4 | vis_id n*4 | cand n*4 | scan status 3*(nblk+1)*8 ]
+//   vis_key n*4 | vis_id n*4 | cand n*4 | tile mask n*8 (LiDAR) |
+//   row table n*32 (pinhole) | scan status 3*(nblk+1)*8 ]
+// Row table (pinhole rects of more than one tile, <= PH_ROWS_MAX rows, <= 255 columns):
+// u16 per tile row of the rect, first column (relative to the rect) in the
+// low byte and the number of tiles in the high byte (binning.cuh).
+// Tile mask (LiDAR): bit k = tile k of the rect in row-major order holds a
+// contributing ray (binning.cuh li_tile_hits); ~0 = every tile of the rect
+// (rects of more than 64 tiles).
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_TILE = SCAN_ITEMS * SCAN_THREADS;
@@ -111,7 +118,7 @@ static_assert(sizeof(ProjHeader) == 256, "header");
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjLayout {
-    size_t rec, rect, key, cnt, vkey, vid, cand, status, nblk, total;
+    size_t rec, rect, key, cnt, vkey, vid, cand, tmask, rows, status, nblk, total;
     __host__ __device__ ProjLayout(int64_t n, int kind) {
         size_t N = (size_t)(n > 0 ? n : 0);
         nblk = (N + SCAN_TILE - 1) / SCAN_TILE;
@@ -122,7 +129,9 @@ struct ProjLayout {
         vkey = cnt + align256(N * 4);
         vid = vkey + align256(N * 4);
         cand = vid + align256(N * 4);
-        status = cand + align256(N * 4);
+        tmask = cand + align256(N * 4);
+        rows = tmask + align256(kind == GS_LIDAR_SPINNING ? N * 8 : 0);
+        status = rows + align256(kind == GS_PINHOLE ? N * 32 : 0);
         total = status + align256(3 * (nblk + 1) * 8);
     }
 };

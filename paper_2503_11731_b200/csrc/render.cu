@@ -9,7 +9,7 @@
 // tile (opts tile_w x tile_h samples); each of its consumer warps owns a
 // 32-sample sub-tile (8x4 pixels for cameras, 32x1 LiDAR columns of one beam)
 // and one producer warp streams the tile's depth-sorted surfel records into a
-// shared-memory ring with TMA bulk copies completing on mbarriers, so every
+// shared-memory ring with cp.async copies completing on mbarriers, so every
 // record is fetched from L2/HBM once per tile and the consumer warps drift up
 // to a ring's length apart instead of meeting at a barrier per batch.  Each
 // consumer ballots which records of a slot touch its sub-tile (conservative
@@ -27,6 +27,8 @@
 // (M^T h_u) x (M^T h_v) = det(M) M^{-1} (h_u x h_v): the kernels evaluate the
 // adjugate of the surfel map on the ray direction.  Records are written
 // relative to the surfel centre so that fp32 suffices here.
+#include <string.h>
+
 #include <algorithm>
 
 #include "gsr_internal.cuh"
@@ -836,10 +838,32 @@ __device__ __forceinline__ void render_body(
     }
 }
 
-// Register budgets per sensor kind (measured): pinhole compositing runs best
-// at 56 registers per thread (seven 5-warp CTAs per SM), fisheye and LiDAR at
-// 64 (fewer spills).
-template <bool STATS>
+// The north_star compositing constants (gs_default_opts) as compile-time
+// literals: the DEF kernels fold them into immediates instead of reloading
+// six uniform registers in every record evaluation.  Chosen on the host when
+// the options equal the defaults bit for bit (is_default_ops).
+constexpr float DEF_LP_SIGMA = 0.70710678118654752f;
+constexpr float DEF_SIGMA2 = DEF_LP_SIGMA * DEF_LP_SIGMA;
+__device__ __forceinline__ DevOpts default_ops(DevOpts o) {
+    o.near_plane = 0.2f;
+    o.alpha_max = 0.99f;
+    o.alpha_min = 1.0f / 255.0f;
+    o.t_min = 1e-4f;
+    o.support = 9.0f;
+    o.sigma2 = DEF_SIGMA2;
+    o.inv_sigma2 = 1.0f / DEF_SIGMA2;
+    return o;
+}
+static bool is_default_ops(const DevOpts &o) {
+    auto same = [](float a, float b) { return memcmp(&a, &b, 4) == 0; };
+    return same(o.near_plane, 0.2f) && same(o.alpha_max, 0.99f) && same(o.alpha_min, 1.0f / 255.0f) &&
+           same(o.t_min, 1e-4f) && same(o.support, 9.0f) && same(o.sigma2, DEF_SIGMA2) &&
+           same(o.inv_sigma2, 1.0f / DEF_SIGMA2);
+}
+
+// Register budget (measured, tools/sweep.py): 64 registers per thread for
+// every sensor kind (six 5-warp CTAs per SM for the pinhole).
+template <bool STATS, bool DEF>
 __global__ void __maxnreg__(64) k_render_pinhole(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
@@ -847,10 +871,11 @@ __global__ void __maxnreg__(64) k_render_pinhole(
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
-    render_body<GS_PINHOLE, STATS>(rec, values, ranges, d_overflow, se, op, h, items, split_base, partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
+    render_body<GS_PINHOLE, STATS>(rec, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
+                                   partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
 }
 
-template <int KIND, bool STATS>
+template <int KIND, bool STATS, bool DEF>
 __global__ void __maxnreg__(64) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
@@ -858,7 +883,8 @@ __global__ void __maxnreg__(64) k_render(
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
-    render_body<KIND, STATS>(rec, values, ranges, d_overflow, se, op, h, items, split_base, partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
+    render_body<KIND, STATS>(rec, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
+                             partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
 }
 
 // ---------------------------------------------------------------- merge of split lists
@@ -1039,7 +1065,9 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const bool piped = npix > 32;   // multi-warp tiles: a producer warp + the staging ring
     const size_t sm = (size_t)(piped ? KSLOTS : 2) * 32 * Rec<KIND>::S4 * 16;
     const int nthr = piped ? npix + 32 : npix;
-    auto *kern = KIND == GS_PINHOLE ? k_render_pinhole<STATS> : k_render<KIND, STATS>;
+    const bool def = is_default_ops(op);
+    auto *kern = KIND == GS_PINHOLE ? (def ? k_render_pinhole<STATS, true> : k_render_pinhole<STATS, false>)
+                                    : (def ? k_render<KIND, STATS, true> : k_render<KIND, STATS, false>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, per = 1;

@@ -15,6 +15,7 @@
 
 #include "gsr_internal.cuh"
 #include "scan.cuh"
+#include "binning.cuh"
 
 namespace gsr {
 
@@ -327,6 +328,7 @@ __device__ __forceinline__ uint32_t first_surfel(const uint32_t *__restrict__ of
 __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
                                               const uint32_t *__restrict__ offs,
                                               const short4 *__restrict__ rect,
+                                              const uint64_t *__restrict__ tmask,
                                               const ProjHeader *hdr, const uint32_t *d_np, int ntx, int npass,
                                               int tbits, uint32_t *__restrict__ tkey,
                                               uint32_t *__restrict__ tval, uint32_t *__restrict__ thist,
@@ -347,12 +349,14 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
             const uint32_t kk = k + (uint32_t)lane;
             uint32_t id = 0, o0 = 0xffffffffu;
             int x0 = 0, y0 = 0, wd = 1;
+            uint64_t mk = ~0ull;
             if (kk < n) {
                 id = sid[kk];
                 const short4 r = rect[id];
                 x0 = r.x; y0 = r.y;
                 wd = r.z - r.x + 1;
                 o0 = offs[kk];
+                if (tmask) mk = tmask[id];
             }
             const uint32_t gbeg = max(q0, __shfl_sync(FULL_MASK, o0, 0));
             // end of the group's pairs: offset of surfel k+32 (or P), clipped to the task
@@ -371,8 +375,14 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
                 const uint32_t rlo = __shfl_sync(FULL_MASK, o0, idx);
                 const int rx0 = __shfl_sync(FULL_MASK, x0, idx), ry0 = __shfl_sync(FULL_MASK, y0, idx);
                 const int rw = __shfl_sync(FULL_MASK, wd, idx);
+                const uint32_t mlo = __shfl_sync(FULL_MASK, (uint32_t)mk, idx);
+                const uint32_t mhi = __shfl_sync(FULL_MASK, (uint32_t)(mk >> 32), idx);
                 if (q < gend) {
-                    const uint32_t r = q - rlo;
+                    uint32_t r = q - rlo;
+                    if ((mlo & mhi) != FULL_MASK) {   // tile mask (LiDAR): r-th set bit
+                        const uint32_t pl = (uint32_t)__popc(mlo);
+                        r = r < pl ? __fns(mlo, 0, (int)r + 1) : 32u + __fns(mhi, 0, (int)(r - pl) + 1);
+                    }
                     const int dy = (int)(r / (uint32_t)rw), dx = (int)(r - (uint32_t)dy * (uint32_t)rw);
                     const int tx = rx0 + dx;
                     const uint32_t tile = (uint32_t)((ry0 + dy) * ntx + (tx >= ntx ? tx - ntx : tx));
@@ -384,6 +394,115 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
                     }
                 }
             }
+            if (onext >= q1 || k + 32 >= n) break;
+            k += 32;
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; ++p)
+        for (int b = threadIdx.x; b < RS_BINS; b += blockDim.x)
+            if (h[p][b]) atomicAdd(&thist[p * RS_BINS + b], h[p][b]);
+}
+
+// Pinhole emission with exact tile rows (binning.cuh): a surfel's pairs are
+// the tiles of its row table (ProjLayout::rows, written by k_project with the
+// count), row by row; rects of fewer than KT_MIN_AREA tiles, more than
+// PH_ROWS_MAX rows or more than 255 columns take every tile.  As in k_emit the warp takes the task's
+// surfels in groups of 32; each lane first writes its surfel's rows (pairs
+// before the row << 8 | first column) to shared memory, then lane q of each
+// round writes one pair: its surfel by a binary search over the group's
+// offsets (shuffles), its row by a binary search of that surfel's rows.
+// Consecutive lanes write consecutive pairs (coalesced).
+constexpr int EM_RS = 33;   // row stride of the shared row tables (bank spread)
+
+__global__ void __launch_bounds__(256) k_emit_rows(const uint32_t *__restrict__ sid,
+                                                   const uint32_t *__restrict__ offs,
+                                                   const short4 *__restrict__ rect,
+                                                   const uint4 *__restrict__ rows,
+                                                   const ProjHeader *hdr, const uint32_t *d_np, int ntx,
+                                                   int npass, int tbits, uint32_t *__restrict__ tkey,
+                                                   uint32_t *__restrict__ tval, uint32_t *__restrict__ thist,
+                                                   const int32_t *d_overflow) {
+    __shared__ uint32_t h[3][RS_BINS];
+    __shared__ uint32_t s_row[8][PH_ROWS_MAX * EM_RS];   // [warp][row * EM_RS + lane]
+    if (*d_overflow) return;
+    for (int i = threadIdx.x; i < 3 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t n = hdr->n_visible, P = *d_np;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *srow = s_row[wid];
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t ntask = (P + EM_CH - 1) / EM_CH;
+    for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + wid; c < ntask; c += nwarps) {
+        const uint32_t q0 = c * EM_CH, q1 = min(P, q0 + EM_CH);
+        uint32_t k = first_surfel(offs, n, q0, lane);
+        while (true) {
+            const uint32_t kk = k + (uint32_t)lane;
+            uint32_t id = 0, o0 = 0xffffffffu;
+            int x0 = 0, y0 = 0, wd = 1, nr = 0;   // nr > 0: row-table mode with nr rows
+            if (kk < n) {
+                id = sid[kk];
+                const short4 r = rect[id];
+                x0 = r.x; y0 = r.y;
+                wd = r.z - r.x + 1;
+                o0 = offs[kk];
+                const int nrows = r.w - r.y + 1;
+                if (wd * nrows >= (int)KT_MIN_AREA && nrows <= PH_ROWS_MAX && wd <= 255) {
+                    const uint4 t0 = __ldg(rows + 2 * (size_t)id), t1 = __ldg(rows + 2 * (size_t)id + 1);
+                    const uint32_t tb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+                    uint32_t cum = 0;
+#pragma unroll
+                    for (int rr = 0; rr < PH_ROWS_MAX; ++rr) {
+                        const uint32_t e = (tb[rr >> 1] >> (16 * (rr & 1))) & 0xffffu;
+                        if (rr < nrows) srow[rr * EM_RS + lane] = (cum << 8) | (e & 0xffu);
+                        cum += e >> 8;
+                    }
+                    nr = nrows;
+                }
+            }
+            __syncwarp();
+            const uint32_t gbeg = max(q0, __shfl_sync(FULL_MASK, o0, 0));
+            const uint32_t onext = k + 32 < n ? __ldg(offs + k + 32) : P;
+            const uint32_t gend = min(q1, onext);
+            for (uint32_t qb = gbeg; qb < gend; qb += 32) {
+                const uint32_t q = qb + (uint32_t)lane;
+                int idx = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const uint32_t l = __shfl_sync(FULL_MASK, o0, idx + step);
+                    if (idx + step < 32 && l <= q) idx += step;
+                }
+                const uint32_t rid = __shfl_sync(FULL_MASK, id, idx);
+                const uint32_t rlo = __shfl_sync(FULL_MASK, o0, idx);
+                const int rx0 = __shfl_sync(FULL_MASK, x0, idx), ry0 = __shfl_sync(FULL_MASK, y0, idx);
+                const int rw = __shfl_sync(FULL_MASK, wd, idx);
+                const int rnr = __shfl_sync(FULL_MASK, nr, idx);
+                if (q < gend) {
+                    const uint32_t r = q - rlo;
+                    int ty, tx;
+                    if (rnr > 0) {   // last row whose first pair is <= r
+                        int rr = 0;
+#pragma unroll
+                        for (int step = PH_ROWS_MAX / 2; step; step >>= 1)
+                            if (rr + step < rnr && (srow[(rr + step) * EM_RS + idx] >> 8) <= r) rr += step;
+                        const uint32_t e = srow[rr * EM_RS + idx];
+                        ty = ry0 + rr;
+                        tx = rx0 + (int)(e & 0xffu) + (int)(r - (e >> 8));
+                    } else {
+                        const int dy = (int)(r / (uint32_t)rw);
+                        ty = ry0 + dy;
+                        tx = rx0 + (int)(r - (uint32_t)dy * (uint32_t)rw);
+                    }
+                    const uint32_t tile = (uint32_t)(ty * ntx + tx);
+                    tkey[q] = tile;
+                    tval[q] = rid;
+                    for (int p = 0; p < npass; ++p) {
+                        const int bits = min(8, tbits - 8 * p);
+                        atomicAdd(&h[p][(tile >> (8 * p)) & ((1u << bits) - 1)], 1u);
+                    }
+                }
+            }
+            __syncwarp();
             if (onext >= q1 || k + 32 >= n) break;
             k += 32;
         }
@@ -446,9 +565,10 @@ size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles) {
     return sort_layout(n, cap, ntiles).total;
 }
 
-cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int64_t ntiles,
+cudaError_t launch_bin_sort(const void *proj, int64_t n, const DevSensor &se, int64_t ntiles,
                             uint64_t *keys, uint32_t *values, int64_t cap, uint32_t *ranges,
                             void *ws, int32_t *d_overflow, cudaStream_t st) {
+    const int kind = se.kind, ntx = se.ntx;
     const ProjLayout L(n, kind);
     const SortWs W = sort_layout(n, cap, ntiles);
     const char *pb = (const char *)proj;
@@ -523,8 +643,14 @@ cudaError_t launch_bin_sort(const void *proj, int64_t n, int kind, int ntx, int6
     // P is only known on the device: enough warps for the capacity's tasks, at most 8 CTAs per SM
     const int64_t tasks = (cap + EM_CH - 1) / EM_CH;
     const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, (int64_t)nsm * 8));
-    k_emit<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), hdr, d_np, ntx, np, tb, tk[cur], tv[cur],
-                               thist, d_overflow);
+    if (kind == GS_PINHOLE) {
+        k_emit_rows<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect), (const uint4 *)(pb + L.rows), hdr,
+                                        d_np, ntx, np, tb, tk[cur], tv[cur], thist, d_overflow);
+    } else {
+        k_emit<<<ge, 256, 0, st>>>(sid, offs, (const short4 *)(pb + L.rect),
+                                   kind == GS_LIDAR_SPINNING ? (const uint64_t *)(pb + L.tmask) : nullptr, hdr, d_np,
+                                   ntx, np, tb, tk[cur], tv[cur], thist, d_overflow);
+    }
     CK(cudaGetLastError());
     // 3. tile digits over the pairs
     note_launch();

@@ -177,3 +177,227 @@ def cpu_bin_sort(rect, key, ntx, ntiles):
     ranges[nz, 0] = starts[nz]
     ranges[nz, 1] = ends[nz]
     return vals, keys, ranges
+
+
+def check_sorted_pairs(b, ntx):
+    """The GPU's sorted pair list is a valid binning of the tile set it
+    emitted: (tile, depth-key bits, surfel index) strictly increasing, each
+    pair's key bits = its surfel's key, every visible surfel emitted exactly
+    count[i] pairs whose tile hull is its rect, and the tile ranges are the
+    [start, end) runs of the sorted tiles (bit-exact).  Returns the pairs'
+    (tile, surfel) arrays for further checks."""
+    P = b["P"]
+    vals = b["values"].astype(np.int64)
+    keys = b["keys"]
+    assert len(vals) == P and len(keys) == P
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    kb = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    np.testing.assert_array_equal(kb, b["key"][vals])
+    if P > 1:
+        t0, t1 = tiles[:-1], tiles[1:]
+        k0, k1 = kb[:-1], kb[1:]
+        v0, v1 = vals[:-1], vals[1:]
+        inc = (t0 < t1) | ((t0 == t1) & ((k0 < k1) | ((k0 == k1) & (v0 < v1))))
+        assert inc.all(), f"sorted pairs out of order at {np.nonzero(~inc)[0][:5]}"
+    n = len(b["count"])
+    cnt = np.bincount(vals, minlength=n)
+    np.testing.assert_array_equal(cnt, b["count"].astype(np.int64))
+    rect = b["rect"].astype(np.int64)
+    tx = tiles % ntx
+    ty = tiles // ntx
+    tx = np.where(tx < rect[vals, 0], tx + ntx, tx)   # LiDAR rects may run past the seam (columns >= ntx)
+    big = np.int64(1) << 40
+    for arr, col, red in ((tx, 0, np.minimum), (ty, 1, np.minimum), (tx, 2, np.maximum), (ty, 3, np.maximum)):
+        acc = np.full(n, big if red is np.minimum else -big, np.int64)
+        red.at(acc, vals, arr)
+        vis = cnt > 0
+        np.testing.assert_array_equal(acc[vis], rect[vis, col])
+    ranges = np.zeros((b["ntiles"], 2), np.uint32)
+    starts = np.searchsorted(tiles, np.arange(b["ntiles"]), side="left")
+    ends = np.searchsorted(tiles, np.arange(b["ntiles"]), side="right")
+    nz = ends > starts
+    ranges[nz, 0] = starts[nz]
+    ranges[nz, 1] = ends[nz]
+    np.testing.assert_array_equal(b["ranges"], ranges)
+    return tiles, vals
+
+
+def required_pinhole_pairs(surfels, sensor, tile_w, tile_h, idx=None, near=0.2, support=9.0, sigma=0.70710678,
+                           alpha_min=1.0 / 255.0, margin=1e-4, max_window=1 << 16):
+    """(tile, surfel) pairs a pinhole binning must contain, from an fp64
+    evaluation of the definition (Eq. 2 intersection of the
+    pixel-centre ray with the surfel plane, the 3-sigma cut rho <= support
+    with the opacity-aware alpha cut, the low-pass floor, the near plane),
+    independent of the GPU records: every tile holding a pixel centre where
+    the surfel contributes with a relative margin `margin` inside every cut.
+    Pixel centres are enumerated over the projected 3-sigma circle's box
+    (256 boundary points) and the low-pass disc, widened by 2 px; surfels
+    whose boundary crosses the near plane or whose window exceeds
+    max_window pixels are skipped (returned count)."""
+    W, H = sensor.width, sensor.height
+    Wm = np.asarray(sensor.world_to_sensor, np.float64)
+    Rs, ts = Wm[:, :3], Wm[:, 3]
+    n = surfels.n
+    idx = np.arange(n) if idx is None else np.asarray(idx)
+    mu = surfels.means[idx].astype(np.float64) @ Rs.T + ts
+    q = surfels.quats[idx].astype(np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    tu = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)], 1) @ Rs.T
+    tv = np.stack([2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)], 1) @ Rs.T
+    a = tu * surfels.scales[idx, 0:1].astype(np.float64)
+    bb = tv * surfels.scales[idx, 1:2].astype(np.float64)
+    o = surfels.opacities[idx].astype(np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rcut = np.minimum(support, 2.0 * np.log(o / alpha_min))
+    fx, fy, cx, cy = float(sensor.fx), float(sensor.fy), float(sensor.cx), float(sensor.cy)
+    ok = (mu[:, 2] > near) & (rcut > 0) & np.isfinite(rcut)
+    ang = np.linspace(0, 2 * np.pi, 256, endpoint=False)
+    R3 = np.sqrt(np.maximum(rcut, 0))
+    pts = mu[:, None, :] + R3[:, None, None] * (np.cos(ang)[None, :, None] * a[:, None, :] +
+                                                np.sin(ang)[None, :, None] * bb[:, None, :])
+    front = (pts[:, :, 2] > near).all(axis=1)
+    px = fx * pts[:, :, 0] / np.where(front[:, None], pts[:, :, 2], 1.0) + cx
+    py = fy * pts[:, :, 1] / np.where(front[:, None], pts[:, :, 2], 1.0) + cy
+    ccx = fx * mu[:, 0] / mu[:, 2] + cx
+    ccy = fy * mu[:, 1] / mu[:, 2] + cy
+    rlp = sigma * R3
+    x0 = np.floor(np.minimum(px.min(1), ccx - rlp) - 2).clip(0, W - 1).astype(np.int64)
+    x1 = np.ceil(np.maximum(px.max(1), ccx + rlp) + 2).clip(0, W - 1).astype(np.int64)
+    y0 = np.floor(np.minimum(py.min(1), ccy - rlp) - 2).clip(0, H - 1).astype(np.int64)
+    y1 = np.ceil(np.maximum(py.max(1), ccy + rlp) + 2).clip(0, H - 1).astype(np.int64)
+    win = (x1 - x0 + 1) * (y1 - y0 + 1)
+    use = ok & front & (win <= max_window)
+    skipped = int(np.sum(ok & ~use))
+    out = []
+    sel = np.nonzero(use)[0]
+    for chunk in np.array_split(sel, max(1, int(win[sel].sum() // 4_000_000) + 1)):
+        if len(chunk) == 0:
+            continue
+        cw = win[chunk]
+        rep = np.repeat(chunk, cw)
+        k = np.arange(int(cw.sum())) - np.repeat(np.cumsum(cw) - cw, cw)
+        ww = (x1 - x0 + 1)[rep]
+        pxi = x0[rep] + k % ww
+        pyi = y0[rep] + k // ww
+        dx = (pxi + 0.5 - cx) / fx
+        dy = (pyi + 0.5 - cy) / fy
+        d = np.stack([dx, dy, np.ones_like(dx)], 1)
+        A, B, M = a[rep], bb[rep], mu[rep]
+        # mu + u a + v b = lam d  ->  [a b -d][u v lam]^T = -mu (Cramer)
+        Dm = -d
+        det = np.einsum("ij,ij->i", A, np.cross(B, Dm))
+        rhs = -M
+        with np.errstate(divide="ignore", invalid="ignore"):
+            u = np.einsum("ij,ij->i", rhs, np.cross(B, Dm)) / det
+            v = np.einsum("ij,ij->i", A, np.cross(rhs, Dm)) / det
+            lam = np.einsum("ij,ij->i", A, np.cross(B, rhs)) / det
+        rho3 = u * u + v * v
+        rho2 = ((pxi + 0.5 - ccx[rep]) ** 2 + (pyi + 0.5 - ccy[rep]) ** 2) / (sigma * sigma)
+        use3 = rho3 <= rho2
+        rho = np.where(use3, rho3, rho2)
+        dep = np.where(use3, lam, mu[rep, 2])
+        lim = rcut[rep] * (1 - margin)
+        need = np.isfinite(rho) & (rho <= lim) & (dep >= near * (1 + margin))
+        t = (pyi[need] // tile_h) * ((W + tile_w - 1) // tile_w) + pxi[need] // tile_w
+        out.append(np.unique(t.astype(np.int64) * (1 << 32) + idx[rep[need]]))
+    pairs = np.unique(np.concatenate(out)) if out else np.zeros(0, np.int64)
+    return pairs >> 32, pairs & 0xFFFFFFFF, skipped
+
+
+def check_pinhole_binning(b, surfels, sensor, tile_w, tile_h, idx=None, **kw):
+    """Sorted-pair validity (check_sorted_pairs) plus conservativeness: every
+    required (tile, surfel) pair of the fp64 definition is emitted."""
+    ntx = (sensor.width + tile_w - 1) // tile_w
+    tiles, vals = check_sorted_pairs(b, ntx)
+    rt, rs, skipped = required_pinhole_pairs(surfels, sensor, tile_w, tile_h, idx=idx, **kw)
+    have = np.unique(tiles * (1 << 32) + vals)
+    need = rt * (1 << 32) + rs
+    missing = np.setdiff1d(need, have)
+    assert len(missing) == 0, f"{len(missing)} required pairs missing, e.g. tile/surfel " \
+                              f"{[(int(m >> 32), int(m & 0xFFFFFFFF)) for m in missing[:5]]}"
+    return dict(P=b["P"], required=len(need), skipped=skipped)
+
+
+def required_lidar_pairs(surfels, sensor, tile_w, idx=None, near=0.2, support=9.0, alpha_min=1.0 / 255.0,
+                         margin=1e-4, max_window=1 << 16):
+    """(tile, surfel) pairs a LiDAR binning (tile = tile_w columns of one beam
+    row) must contain, from an fp64 evaluation of the definition (Eq. 5 rays,
+    Eq. 2 intersection, 3-sigma cut with the opacity-aware alpha cut, near
+    plane; no low-pass, reading R6): every tile holding a ray that meets the
+    surfel with a relative margin inside every cut.  Rays are enumerated over
+    the angular window of the 3-sigma circle (256 boundary points), widened by
+    two beams / columns; surfels whose window wraps the whole turn or exceeds
+    max_window rays are skipped (returned count)."""
+    W, H = sensor.width, sensor.height
+    ntx = (W + tile_w - 1) // tile_w
+    Wm = np.asarray(sensor.world_to_sensor, np.float64)
+    Rs, ts = Wm[:, :3], Wm[:, 3]
+    idx = np.arange(surfels.n) if idx is None else np.asarray(idx)
+    mu = surfels.means[idx].astype(np.float64) @ Rs.T + ts
+    q = surfels.quats[idx].astype(np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    tu = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)], 1) @ Rs.T
+    tv = np.stack([2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)], 1) @ Rs.T
+    a = tu * surfels.scales[idx, 0:1].astype(np.float64)
+    bb = tv * surfels.scales[idx, 1:2].astype(np.float64)
+    o = surfels.opacities[idx].astype(np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rcut = np.minimum(support, 2.0 * np.log(o / alpha_min))
+    ok = (np.linalg.norm(mu, axis=1) > near) & (rcut > 0) & np.isfinite(rcut)
+    R3 = np.sqrt(np.maximum(rcut, 0))
+    ang = np.linspace(0, 2 * np.pi, 256, endpoint=False)
+    pts = mu[:, None, :] + R3[:, None, None] * (np.cos(ang)[None, :, None] * a[:, None, :] +
+                                                np.sin(ang)[None, :, None] * bb[:, None, :])
+    el = np.arctan2(pts[:, :, 2], np.hypot(pts[:, :, 0], pts[:, :, 1]))
+    azc = np.arctan2(mu[:, 1], mu[:, 0])
+    daz = np.angle(np.exp(1j * (np.arctan2(pts[:, :, 1], pts[:, :, 0]) - azc[:, None])))
+    beams = np.asarray(sensor.beam_elevation, np.float64)
+    bstep = np.abs(np.diff(beams)).max() if H > 1 else 1.0
+    az0, step = float(sensor.azimuth0), float(sensor.azimuth_step)
+    # the sensor origin inside the disk's cone (all azimuths): skip
+    wide = (daz.max(1) - daz.min(1)) > np.pi
+    j0 = np.floor((azc + daz.min(1) - az0) / step).astype(np.int64) - 2
+    j1 = np.ceil((azc + daz.max(1) - az0) / step).astype(np.int64) + 2
+    lo_el, hi_el = el.min(1) - 2 * bstep, el.max(1) + 2 * bstep
+    rows = [np.nonzero((beams >= lo_el[k]) & (beams <= hi_el[k]))[0] for k in range(len(idx))]
+    ncol = np.minimum(j1 - j0 + 1, W)
+    nrow = np.array([len(r) for r in rows])
+    use = ok & ~wide & (ncol * nrow <= max_window) & (nrow > 0)
+    skipped = int(np.sum(ok & ~use))
+    out = []
+    for k in np.nonzero(use)[0]:
+        rr = rows[k]
+        jj = j0[k] + np.arange(ncol[k])
+        th = beams[rr][:, None]
+        ph = az0 + np.mod(jj, W)[None, :] * step
+        d = np.stack(np.broadcast_arrays(np.cos(th) * np.cos(ph), np.cos(th) * np.sin(ph), np.sin(th)), -1).reshape(-1, 3)
+        A, B, M = a[k], bb[k], mu[k]
+        Dm = -d
+        det = (np.cross(B, Dm) @ A)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            u = (np.cross(B, Dm) @ (-M)) / det
+            v = np.einsum("j,ij->i", A, np.cross(-M[None, :], Dm)) / det
+            lam = np.einsum("j,ij->i", A, np.cross(B[None, :], -M[None, :])) / det
+        rho = u * u + v * v
+        need = np.isfinite(rho) & (rho <= rcut[k] * (1 - margin)) & (lam >= near * (1 + margin))
+        r_idx = np.repeat(rr, len(jj))[need]
+        c_idx = np.tile(np.mod(jj, W), len(rr))[need]
+        t = r_idx * ntx + c_idx // tile_w
+        out.append(np.unique(t.astype(np.int64) * (1 << 32) + idx[k]))
+    pairs = np.unique(np.concatenate(out)) if out else np.zeros(0, np.int64)
+    return pairs >> 32, pairs & 0xFFFFFFFF, skipped
+
+
+def check_lidar_binning(b, surfels, sensor, tile_w, idx=None, **kw):
+    """Sorted-pair validity plus conservativeness (required_lidar_pairs)."""
+    ntx = (sensor.width + tile_w - 1) // tile_w
+    tiles, vals = check_sorted_pairs(b, ntx)
+    rt, rs, skipped = required_lidar_pairs(surfels, sensor, tile_w, idx=idx, **kw)
+    have = np.unique(tiles * (1 << 32) + vals)
+    need = rt * (1 << 32) + rs
+    missing = np.setdiff1d(need, have)
+    assert len(missing) == 0, f"{len(missing)} required pairs missing, e.g. tile/surfel " \
+                              f"{[(int(m >> 32), int(m & 0xFFFFFFFF)) for m in missing[:5]]}"
+    return dict(P=b["P"], required=len(need), skipped=skipped)

@@ -132,11 +132,7 @@ def test_exact_depth_key_ties(gsr_mod):
     _check(s, se, label="ties")
     img, r = _render(s, se, keys=True)
     b = r.binning_state()
-    ntx = (se.width + r.cam_opts.tile_w - 1) // r.cam_opts.tile_w
-    vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
-    np.testing.assert_array_equal(b["values"], vals)
-    np.testing.assert_array_equal(b["keys"], keys)
-    np.testing.assert_array_equal(b["ranges"], ranges)
+    parity.check_pinhole_binning(b, s, se, r.cam_opts.tile_w, r.cam_opts.tile_h)
 
 
 @pytest.mark.parametrize("kind", ["pinhole", "lidar"])
@@ -192,10 +188,11 @@ def test_render_workspace_too_small_gives_background(gsr_mod):
 # ---------------------------------------------------------------- bench scale binning
 @pytest.mark.slow
 def test_binning_bit_exact_full_chunked_forward_frame(gsr_mod):
-    """The Chunked forward camera of timestep 32 (12 M surfels, ~34 M pairs
-    over 16,200 tiles): keys, values and tile ranges bit-exact against a CPU
-    stable sort of the GPU's own per-surfel (rect, key) arrays; GPU keys equal
-    the oracle's pinned keys."""
+    """The Chunked forward camera of timestep 32 (12 M surfels, ~20 M pairs
+    over 16,200 tiles with exact tile rows): the sorted pairs are a valid
+    stable binning of the emitted set (tests/parity.check_sorted_pairs, tile
+    ranges bit-exact), every required fp64 pair of 300 K sampled surfels is
+    emitted; GPU keys equal the oracle's pinned keys."""
     from paper_2503_11731_b200.render import Renderer, to_device
     s = sg.chunked_surfels()
     se = sg.chunked_timestep_sensors(32)[0]
@@ -203,13 +200,12 @@ def test_binning_bit_exact_full_chunked_forward_frame(gsr_mod):
     r.render(se, keys=True)
     torch.cuda.synchronize()
     b = r.binning_state()
-    assert b["P"] > 20_000_000
-    ntx = (se.width + r.cam_opts.tile_w - 1) // r.cam_opts.tile_w
-    vals, keys, ranges = parity.cpu_bin_sort(b["rect"], b["key"], ntx, b["ntiles"])
-    assert b["P"] == len(vals)
-    np.testing.assert_array_equal(b["values"], vals)
-    np.testing.assert_array_equal(b["keys"], keys)
-    np.testing.assert_array_equal(b["ranges"], ranges)
+    assert b["P"] > 10_000_000
+    # sort validity over all pairs; conservativeness on a sample of 300 K surfels
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(s.n, 300_000, replace=False))
+    st = parity.check_pinhole_binning(b, s, se, r.cam_opts.tile_w, r.cam_opts.tile_h, idx=idx)
+    print("binning chunked forward", st)
     okb, cul = oracle.keys(s, se)
     vis = b["count"] > 0
     np.testing.assert_array_equal(b["key"][vis], okb[vis])
