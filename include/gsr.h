@@ -162,8 +162,8 @@ int64_t gs_num_tiles(const gs_sensor *sensor, const gs_opts *opts);
  * the columns the support conic / disc meets (widened by a slack above the
  * compositor's fp32 error); LiDAR (one-row tiles), per tile a conservative
  * minimum of the support quadric over the tile's ray arc; fisheye, the
- * conservative 3-sigma rectangle of tiles.  The stored rect is the hull of
- * the set.  Then compacts the visible surfels and counts the (tile, surfel)
+ * conservative 3-sigma rectangle of tiles.  The stored rect contains the
+ * set.  Then compacts the visible surfels and counts the (tile, surfel)
  * pairs (the sizes of those sets).
  *   projected       device buffer of >= gs_projected_bytes(n, kind) bytes (out)
  *   d_num_pairs     device int64 (out): total number of pairs P

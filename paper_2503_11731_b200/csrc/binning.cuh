@@ -32,9 +32,8 @@ struct PhRows {
 };
 
 constexpr int PH_ROWS_MIN_SPAN = 4;   // boxes spanning <= this many px (width + height): whole rows
-// Pinhole rects of fewer tiles keep every tile (they could drop little); a
-// pinhole set whose hull has fewer tiles is counted and emitted as its whole
-// hull.  (LiDAR: LI_MIN_AREA in project.cu.)
+// Pinhole rects of fewer tiles keep every tile (they could drop little).
+// (LiDAR: LI_MIN_AREA in project.cu.)
 constexpr uint32_t KT_MIN_AREA = 4;
 constexpr int PH_ROWS_MAX = 16;       // rects of more tile rows (or wider than 255 tiles): every tile of the rect
 __device__ __forceinline__ float bin_sqrt(float x) {

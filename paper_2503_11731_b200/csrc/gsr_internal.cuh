@@ -95,9 +95,9 @@ __host__ __device__ inline int record_floats(int kind) {
 // [ header 256 B | records n*rec | rect n*8 | key n*4 | count n*4 |
 //   vis_key n*4 | vis_id n*4 | cand n*4 | tile mask n*8 (LiDAR) |
 //   row table n*32 (pinhole) | scan status 3*(nblk+1)*8 ]
-// Row table (pinhole rects of more than one tile, <= PH_ROWS_MAX rows, <= 255 columns):
-// u16 per tile row of the rect, first column (relative to the rect) in the
-// low byte and the number of tiles in the high byte (binning.cuh).
+// Row table (pinhole rects of >= KT_MIN_AREA tiles, <= PH_ROWS_MAX rows, <= 255
+// columns): u16 per tile row of the rect, first column (relative to the rect)
+// in the low byte and the number of tiles in the high byte (binning.cuh).
 // Tile mask (LiDAR): bit k = tile k of the rect in row-major order holds a
 // contributing ray (binning.cuh li_tile_hits); ~0 = every tile of the rect
 // (rects of more than 64 tiles).

@@ -812,52 +812,27 @@ __device__ __forceinline__ void project_one(const DevSurfels &s, const DevSensor
             dst[k] = make_float4(R[4 * k], R[4 * k + 1], R[4 * k + 2], R[4 * k + 3]);
         // exact tile rows (binning.cuh), from the record floats in registers: the pair
         // count becomes the number of tiles whose pixel centres the support conic or
-        // the low-pass disc can reach, the rect shrinks to their hull, and the row
-        // table (first column, width per tile row of the shrunk rect) goes to
-        // k_emit_rows.  Measured against a separate load-balanced pass that re-read
-        // the records: 0.03 ms faster per forward / side camera frame.
+        // the low-pass disc can reach, and the row table (first column relative to the
+        // rect | width << 8, one u16 per tile row) goes to k_emit_rows.  Measured
+        // against a separate load-balanced pass that re-read the records: 0.03 ms
+        // faster per forward / side camera frame.
         if ((uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) >= KT_MIN_AREA && ty1 - ty0 + 1 <= PH_ROWS_MAX &&
             tx1 - tx0 + 1 <= 255) {
             const PhRows pr = ph_rows_setup(make_float4(R[0], R[1], R[2], R[3]), make_float4(R[4], R[5], R[6], R[7]),
                                             make_float4(R[8], R[9], R[10], R[11]), R[PH_RCUT2],
                                             __float_as_uint(R[PH_BBX]), __float_as_uint(R[PH_BBY]));
-            uint32_t cnt = 0, tb[PH_ROWS_MAX / 2];
-            int nx0 = 0x7fff, nx1 = -1, ny0 = 0x7fff, ny1 = -1;
-#pragma unroll
-            for (int k = 0; k < PH_ROWS_MAX / 2; ++k) tb[k] = 0;
-            uint32_t ab[PH_ROWS_MAX];
+            uint16_t *tbl = reinterpret_cast<uint16_t *>(rows + 2 * i);
+            uint32_t cnt = 0;
 #pragma unroll 1
             for (int ty = ty0; ty <= ty1; ++ty) {
                 int a, b;
                 ph_row_tiles(pr, ty, tx0, tx1, se.width, se.height, se.tw, se.th, se.mtw, a, b);
-                ab[ty - ty0] = a <= b ? ((uint32_t)a | ((uint32_t)b << 16)) : 0xffffu;
-                if (a <= b) {
-                    cnt += (uint32_t)(b - a + 1);
-                    nx0 = min(nx0, a); nx1 = max(nx1, b);
-                    ny0 = min(ny0, ty); ny1 = ty;
-                }
+                const uint32_t w = a <= b ? (uint32_t)(b - a + 1) : 0u;
+                tbl[ty - ty0] = (uint16_t)((a <= b ? (uint32_t)(a - tx0) : 0u) | (w << 8));
+                cnt += w;
             }
-            // a hull below KT_MIN_AREA tiles is emitted whole (k_emit_rows): count it whole
-            // (it differs from the set only where a middle row came out empty)
-            if (cnt > 0 && (uint32_t)((nx1 - nx0 + 1) * (ny1 - ny0 + 1)) < KT_MIN_AREA)
-                cnt = (uint32_t)((nx1 - nx0 + 1) * (ny1 - ny0 + 1));
-            if (cnt == 0) {
-                keys[i] = 0xffffffffu;
-                counts[i] = 0;
-            } else {
-#pragma unroll 1
-                for (int ty = ny0; ty <= ny1; ++ty) {
-                    const uint32_t e = ab[ty - ty0];
-                    const uint32_t ent = e == 0xffffu ? 0u : (((e & 0xffffu) - (uint32_t)nx0) |
-                                                              (((e >> 16) - (e & 0xffffu) + 1u) << 8));
-                    const int k = ty - ny0;
-                    tb[k >> 1] |= ent << (16 * (k & 1));
-                }
-                rows[2 * i] = make_uint4(tb[0], tb[1], tb[2], tb[3]);
-                rows[2 * i + 1] = make_uint4(tb[4], tb[5], tb[6], tb[7]);
-                counts[i] = cnt;
-                rect[i] = make_short4((short)nx0, (short)ny0, (short)nx1, (short)ny1);
-            }
+            if (cnt == 0) keys[i] = 0xffffffffu;
+            counts[i] = cnt;
         }
     } else {
         constexpr int NF = dir_camera(KIND) ? FE_FLOATS : LI_FLOATS;
@@ -938,9 +913,8 @@ __global__ void __launch_bounds__(256, KIND == GS_LIDAR_SPINNING ? PROJ_MINB_LID
 // ------------------------------------------------------------------ exact LiDAR tile sets
 // After k_project (binning.cuh li_tile_hits): per tile of the rect (one-row
 // tiles, rects of LI_MIN_AREA..64 tiles) the support-quadric test over the
-// tile's ray arc, stored as a mask over the shrunk rect; the count becomes
-// the number of admitted tiles, the rect their hull (an empty set culls the
-// surfel).  Load-balanced: a warp takes 32 candidates, stages their record
+// tile's ray arc, stored as a mask over the rect; the count becomes the
+// number of admitted tiles (an empty set culls the surfel).  Load-balanced: a warp takes 32 candidates, stages their record
 // quantities in shared memory and deals their (surfel, tile) items over its
 // lanes 32 at a time; tile-column and beam-row trig come from per-CTA shared
 // tables.  (The pinhole rows are computed inside k_project.)
@@ -1032,33 +1006,12 @@ __global__ void __launch_bounds__(256) k_tiles(const __grid_constant__ DevSensor
         }
         __syncwarp();
         if (nitem == 0) continue;
-        // this lane's surfel: count, hull, and the mask re-indexed over the shrunk rect
+        // this lane's surfel: count and mask (over its rect, row-major)
         const uint64_t bits = (uint64_t)s_res[wid][0][lane] | ((uint64_t)s_res[wid][1][lane] << 32);
         const uint32_t cnt = (uint32_t)__popcll(bits);
-        if (cnt == 0) {
-            keys[i] = 0xffffffffu;
-            counts[i] = 0;
-            continue;
-        }
-        const int w = r.z - r.x + 1, h = r.w - r.y + 1;
-        const uint64_t rm = w >= 64 ? ~0ull : (1ull << w) - 1;
-        int nx0 = 0x7fff, nx1 = -1, ny0 = 0x7fff, ny1 = -1;
-#pragma unroll 1
-        for (int dy = 0; dy < h; ++dy) {
-            const uint64_t rb = (bits >> (dy * w)) & rm;
-            if (rb) {
-                nx0 = min(nx0, r.x + __ffsll((long long)rb) - 1);
-                nx1 = max(nx1, r.x + 63 - __clzll((long long)rb));
-                ny0 = min(ny0, r.y + dy); ny1 = r.y + dy;
-            }
-        }
-        const int nw = nx1 - nx0 + 1;
-        uint64_t mk = 0;
-#pragma unroll 1
-        for (int ty = ny0; ty <= ny1; ++ty) mk |= ((bits >> ((ty - r.y) * w)) & rm) >> (nx0 - r.x) << ((ty - ny0) * nw);
-        tmask[i] = mk;
+        tmask[i] = bits;
         counts[i] = cnt;
-        rect[i] = make_short4((short)nx0, (short)ny0, (short)nx1, (short)ny1);
+        if (cnt == 0) keys[i] = 0xffffffffu;
     }
 }
 

@@ -297,10 +297,25 @@ __device__ __forceinline__ bool rec_hits(const float4 *__restrict__ r, const Sub
     return fmaf(ddx, ddx, ddy * ddy) <= fmaf(r2, 1.0001f, 1e-3f);
 }
 
+// A staged record addressed by its 32-bit shared-memory address: the walk
+// keeps one base register per slot and forms each record's address with one
+// multiply-add (with a generic pointer the compiler re-derived it from the
+// slot and bit index on every iteration).
+struct SmemRec {
+    uint32_t a;
+    __device__ __forceinline__ float4 operator[](int k) const {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "r"(a + 16u * (uint32_t)k));
+        return v;
+    }
+};
+
 // One (sample, surfel) evaluation in list order.  Returns false once the ray
 // stops (the surfel that would push T below t_min is not composited, R3).
-template <int KIND, bool STATS>
-__device__ __forceinline__ bool eval_record(const float4 *__restrict__ r, const Ray &ry, const DevOpts &op,
+template <int KIND, bool STATS, typename RP>
+__device__ __forceinline__ bool eval_record(const RP r, const Ray &ry, const DevOpts &op,
                                             Acc &a, uint32_t &n_eval, uint32_t &n_comp) {
     if (STATS) {   // the sample lies in the record's conservative support region
         constexpr int BB4 = Rec<KIND>::BB / 4;
@@ -490,15 +505,21 @@ __device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restric
                                           uint32_t &n_eval, uint32_t &n_comp) {
     constexpr int S4 = Rec<KIND>::S4;
     if constexpr (KIND == GS_PINHOLE) {   // sparse masks (after the ellipse test): one set bit at a time
+        uint32_t base = (uint32_t)__cvta_generic_to_shared(buf);
+        asm("" : "+r"(base));   // keep the slot base in a register
+        bool stop = false;
 #pragma unroll 1
         while (bits) {
-            const int u = __ffs(bits) - 1;
+            const uint32_t u = (uint32_t)__ffs(bits) - 1u;
             bits &= bits - 1;
-            if (!eval_record<KIND, STATS>(buf + u * S4, ry, op, a, n_eval, n_comp)) {
-                done = true;
-                stopped = true;
-                return;
+            if (!eval_record<KIND, STATS>(SmemRec{base + u * (uint32_t)(S4 * 16)}, ry, op, a, n_eval, n_comp)) {
+                stop = true;
+                break;
             }
+        }
+        if (stop) {
+            done = true;
+            stopped = true;
         }
     } else {
 #pragma unroll 1

@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t *__restrict__ sid,
 // Pinhole emission with exact tile rows (binning.cuh): a surfel's pairs are
 // the tiles of its row table (ProjLayout::rows, written by k_project with the
 // count), row by row; rects of fewer than KT_MIN_AREA tiles, more than
-// PH_ROWS_MAX rows or more than 255 columns take every tile.  As in k_emit the warp takes the task's
+// PH_ROWS_MAX rows or more than 255 columns take every tile (the same test
+// on the same rect as in k_project).  As in k_emit the warp takes the task's
 // surfels in groups of 32; each lane first writes its surfel's rows (pairs
 // before the row << 8 | first column) to shared memory, then lane q of each
 // round writes one pair: its surfel by a binary search over the group's

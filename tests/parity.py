@@ -183,7 +183,7 @@ def check_sorted_pairs(b, ntx):
     """The GPU's sorted pair list is a valid binning of the tile set it
     emitted: (tile, depth-key bits, surfel index) strictly increasing, each
     pair's key bits = its surfel's key, every visible surfel emitted exactly
-    count[i] pairs whose tile hull is its rect, and the tile ranges are the
+    count[i] distinct pairs inside its rect, and the tile ranges are the
     [start, end) runs of the sorted tiles (bit-exact).  Returns the pairs'
     (tile, surfel) arrays for further checks."""
     P = b["P"]
@@ -206,12 +206,11 @@ def check_sorted_pairs(b, ntx):
     tx = tiles % ntx
     ty = tiles // ntx
     tx = np.where(tx < rect[vals, 0], tx + ntx, tx)   # LiDAR rects may run past the seam (columns >= ntx)
-    big = np.int64(1) << 40
-    for arr, col, red in ((tx, 0, np.minimum), (ty, 1, np.minimum), (tx, 2, np.maximum), (ty, 3, np.maximum)):
-        acc = np.full(n, big if red is np.minimum else -big, np.int64)
-        red.at(acc, vals, arr)
-        vis = cnt > 0
-        np.testing.assert_array_equal(acc[vis], rect[vis, col])
+    inside = (tx >= rect[vals, 0]) & (tx <= rect[vals, 2]) & (ty >= rect[vals, 1]) & (ty <= rect[vals, 3])
+    assert inside.all(), f"{int((~inside).sum())} pairs outside their surfel's rect"
+    if len(vals):   # each (tile, surfel) pair once
+        u = np.unique(tiles * (1 << 32) + vals)
+        assert len(u) == len(vals), "duplicate (tile, surfel) pairs"
     ranges = np.zeros((b["ntiles"], 2), np.uint32)
     starts = np.searchsorted(tiles, np.arange(b["ntiles"]), side="left")
     ends = np.searchsorted(tiles, np.arange(b["ntiles"]), side="right")
