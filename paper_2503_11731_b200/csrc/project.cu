@@ -383,24 +383,20 @@ template <int KIND>
 __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op, int64_t i,
                                          uint32_t &keybits, const float *sb) {
     const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1), mz = __ldg(s.means + 3 * i + 2);
-    float keyf;
-    if (KIND == GS_PINHOLE) {
-        keyf = (float)pinned_row(se.R + 6, se.t[2], mx, my, mz);
-    } else {
-        const double a = pinned_row(se.R + 0, se.t[0], mx, my, mz);
-        const double b = pinned_row(se.R + 3, se.t[1], mx, my, mz);
-        const double c = pinned_row(se.R + 6, se.t[2], mx, my, mz);
-        keyf = (float)__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
-    }
-    keybits = __float_as_uint(keyf);
-    const float o = __ldg(s.opac + i);
-    const float2 sc = __ldg(reinterpret_cast<const float2 *>(s.scales) + i);
-    if (!(keyf >= op.near_plane) || !(o > 0.f) || !(sc.x > 0.f) || !(sc.y > 0.f) || !isfinite(sc.x) ||
-        !isfinite(sc.y))
-        return false;
     const float X = fmaf(se.R[0], mx, fmaf(se.R[1], my, fmaf(se.R[2], mz, se.t[0])));
     const float Y = fmaf(se.R[3], mx, fmaf(se.R[4], my, fmaf(se.R[5], mz, se.t[1])));
     const float Z = fmaf(se.R[6], mx, fmaf(se.R[7], my, fmaf(se.R[8], mz, se.t[2])));
+    // conservative near-plane test in fp32: k_project applies the exact one (the pinned
+    // fp64 key, reading R9) to the candidates; the margin covers the fp32 rounding here
+    const float mag = fabsf(mx) + fabsf(my) + fabsf(mz) + fabsf(se.t[0]) + fabsf(se.t[1]) + fabsf(se.t[2]);
+    const float nearm = op.near_plane - fmaf(1e-5f, mag, 1e-6f);
+    const float keyf = KIND == GS_PINHOLE ? Z : sqrtf(fmaf(X, X, fmaf(Y, Y, Z * Z)));
+    keybits = __float_as_uint(keyf);
+    const float o = __ldg(s.opac + i);
+    const float2 sc = __ldg(reinterpret_cast<const float2 *>(s.scales) + i);
+    if (!(keyf >= nearm) || !(o > 0.f) || !(sc.x > 0.f) || !(sc.y > 0.f) || !isfinite(sc.x) ||
+        !isfinite(sc.y))
+        return false;
     const float R = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f) * fmaxf(sc.x, sc.y) +
                     1e-3f * (1.f + fabsf(X) + fabsf(Y) + fabsf(Z));
     if (!isfinite(X + Y + Z + R)) return true;   // let k_project decide

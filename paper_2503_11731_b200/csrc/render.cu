@@ -57,7 +57,10 @@ constexpr float LOG2E_HALF = 0.72134752044448170368f;   // 0.5 * log2(e)
 constexpr int NB = 32;                                   // schedule buckets
 constexpr int NPART = 10;                                // floats per partial composite
 constexpr uint32_t LMIN = 1024;   // shortest segment of the adaptive split (workspace sizing)
-constexpr int NCP = 4;            // checkpoints per split segment (the re-walk covers one fifth)
+#ifndef GSR_NCP
+#define GSR_NCP 4
+#endif
+constexpr int NCP = GSR_NCP;      // checkpoints per split segment (the re-walk covers one fifth)
 constexpr uint32_t NO_STOP = 0xffffffffu;
 constexpr unsigned FULL = 0xffffffffu;
 
