@@ -63,11 +63,12 @@ __device__ __forceinline__ PhRows ph_rows_setup(const float4 g0, const float4 g1
     if ((bx1 - bx0) + (by1 - by0) <= PH_ROWS_MIN_SPAN) { p.full = true; return p; }
     const float R = g1.w, qc = g1.z, ax = g1.x, ay = g1.y;
     const float Rax = __fmul_rn(R, ax), Ray = __fmul_rn(R, ay);
-    const float M00 = __fmaf_rn(g0.x, g0.x, __fmaf_rn(g0.z, g0.z, -__fmul_rn(Rax, ax)));
-    const float M11 = __fmaf_rn(g0.y, g0.y, __fmaf_rn(g0.w, g0.w, -__fmul_rn(Ray, ay)));
-    const float M01 = __fmaf_rn(g0.x, g0.y, __fmaf_rn(g0.z, g0.w, -__fmul_rn(Rax, ay)));
-    const float t00 = __fmaf_rn(g0.x, g0.x, __fmaf_rn(g0.z, g0.z, __fmul_rn(Rax, ax)));
-    const float t11 = __fmaf_rn(g0.y, g0.y, __fmaf_rn(g0.w, g0.w, __fmul_rn(Ray, ay)));
+    // g0 = (A00, A10, A01, A11)
+    const float M00 = __fmaf_rn(g0.x, g0.x, __fmaf_rn(g0.y, g0.y, -__fmul_rn(Rax, ax)));
+    const float M11 = __fmaf_rn(g0.z, g0.z, __fmaf_rn(g0.w, g0.w, -__fmul_rn(Ray, ay)));
+    const float M01 = __fmaf_rn(g0.x, g0.z, __fmaf_rn(g0.y, g0.w, -__fmul_rn(Rax, ay)));
+    const float t00 = __fmaf_rn(g0.x, g0.x, __fmaf_rn(g0.y, g0.y, __fmul_rn(Rax, ax)));
+    const float t11 = __fmaf_rn(g0.z, g0.z, __fmaf_rn(g0.w, g0.w, __fmul_rn(Ray, ay)));
     const float det = __fmaf_rn(M00, M11, -__fmul_rn(M01, M01));
     // well-conditioned only: no cancellation in M00, M11 or det beyond 1e-3 of their terms
     if (!(M00 > __fmul_rn(1e-3f, t00)) || !(M11 > __fmul_rn(1e-3f, t11)) || !(det > __fmul_rn(1e-3f, __fmul_rn(M00, M11)))) {

@@ -46,12 +46,13 @@ struct DevSurfels {
 // memory by the compositing kernels (16-byte chunks).
 //
 // Pinhole (24 floats): the intersection of pixel p = c + (dx,dy) with the
-// surfel is (u,v) = (q0,q1)/q2, camera z = det/q2, where
+// surfel is (u,v) = (q0,q1)/q2, camera z = det/q2 (the A entries column-major,
+// so that (q0, q1) is one packed f32x2 multiply-add per column), where
 //   q0 = A00 dx + A01 dy, q1 = A10 dx + A11 dy, q2 = qc + A20 dx + A21 dy
 // (the first two columns of adj(K M) scaled by 1/(s_u s_v); c the projected
 // centre, stored hi+lo).  See DESIGN.md §6.
 enum : int {
-    PH_A00 = 0, PH_A01, PH_A10, PH_A11, PH_A20, PH_A21, PH_QC, PH_RCUT3,
+    PH_A00 = 0, PH_A10, PH_A01, PH_A11, PH_A20, PH_A21, PH_QC, PH_RCUT3,
     PH_CHX = 8, PH_CHY, PH_CLX, PH_CLY, PH_RCUT2, PH_O, PH_DET, PH_ZC,
     PH_R = 16, PH_G, PH_B, PH_NX, PH_NY, PH_NZ, PH_BBX, PH_BBY, PH_FLOATS = 24
 };

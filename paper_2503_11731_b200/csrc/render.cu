@@ -53,6 +53,31 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Packed fp32 pairs (sm_100 f32x2 add / sub / mul / fma: two independent
+// IEEE fp32 operations per instruction, the same roundings as the scalar ones).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk(f2 r, float &a, float &b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 constexpr float LOG2E_HALF = 0.72134752044448170368f;   // 0.5 * log2(e)
 constexpr int NB = 32;                                   // schedule buckets
 constexpr int NPART = 10;                                // floats per partial composite
@@ -252,13 +277,14 @@ constexpr int ELL_MIN = 4;   // boxes spanning <= this many px (width + height) 
 __device__ __forceinline__ bool ellipse_hits(const float4 *__restrict__ r, float cx, float cy, const SubTile &st) {
     const float4 g0 = r[0], g1 = r[1];
     const float R = g1.w, qc = g1.z;
-    const float M00 = fmaf(g0.x, g0.x, fmaf(g0.z, g0.z, -R * g1.x * g1.x));
-    const float M11 = fmaf(g0.y, g0.y, fmaf(g0.w, g0.w, -R * g1.y * g1.y));
-    const float M01 = fmaf(g0.x, g0.y, fmaf(g0.z, g0.w, -R * g1.x * g1.y));
+    // g0 = (A00, A10, A01, A11)
+    const float M00 = fmaf(g0.x, g0.x, fmaf(g0.y, g0.y, -R * g1.x * g1.x));
+    const float M11 = fmaf(g0.z, g0.z, fmaf(g0.w, g0.w, -R * g1.y * g1.y));
+    const float M01 = fmaf(g0.x, g0.z, fmaf(g0.y, g0.w, -R * g1.x * g1.y));
     const float det = fmaf(M00, M11, -M01 * M01);
     // well-conditioned only: no cancellation in M00, M11 or det beyond 1e-3 of their terms
-    const float t00 = fmaf(g0.x, g0.x, fmaf(g0.z, g0.z, R * g1.x * g1.x));
-    const float t11 = fmaf(g0.y, g0.y, fmaf(g0.w, g0.w, R * g1.y * g1.y));
+    const float t00 = fmaf(g0.x, g0.x, fmaf(g0.y, g0.y, R * g1.x * g1.x));
+    const float t11 = fmaf(g0.z, g0.z, fmaf(g0.w, g0.w, R * g1.y * g1.y));
     if (!(M00 > 1e-3f * t00) || !(M11 > 1e-3f * t11) || !(det > 1e-3f * M00 * M11)) return true;
     const float B0 = -R * qc * g1.x, B1 = -R * qc * g1.y, C = -R * qc * qc;
     const float X0 = (float)st.x0 + 0.49f - cx, X1 = (float)st.x1 + 0.51f - cx;
@@ -334,10 +360,11 @@ __device__ __forceinline__ bool eval_record(const RP r, const Ray &ry, const Dev
     float rho, dep, o;
     if (KIND == GS_PINHOLE) {
         const float4 g0 = r[0], g1 = r[1], g2 = r[2], g3 = r[3];
-        const float dx = (ry.px - g2.x) - g2.z, dy = (ry.py - g2.y) - g2.w;
+        // (dx, dy) = (p - c_hi) - c_lo; (q0, q1) = A01 (dx, dy), A column-major in g0
+        float dx, dy, q0, q1;
+        upk(sub2(sub2(pk(ry.px, ry.py), pk(g2.x, g2.y)), pk(g2.z, g2.w)), dx, dy);
+        upk(fma2(pk(g0.x, g0.y), pk(dx, dx), mul2(pk(g0.z, g0.w), pk(dy, dy))), q0, q1);
         const float s2 = fmaf(dx, dx, dy * dy);
-        const float q0 = fmaf(g0.x, dx, g0.y * dy);
-        const float q1 = fmaf(g0.z, dx, g0.w * dy);
         const float q2 = fmaf(g1.x, dx, fmaf(g1.y, dy, g1.z));
         const float n3 = fmaf(q0, q0, q1 * q1);
         if ((n3 > g1.w * q2 * q2) && (s2 > g3.x)) return true;
@@ -387,9 +414,14 @@ __device__ __forceinline__ bool eval_record(const RP r, const Ray &ry, const Dev
         const float4 p = r[5];
         a.c0 = fmaf(w, p.x, a.c0);   // intensity
         a.c1 = fmaf(w, p.y, a.c1);   // ray-drop probability
+    } else if (KIND == GS_PINHOLE) {   // packed: (c0,c1) (c2,n0) (n1,n2) += w (r,g) (b,nx) (ny,nz)
+        const float4 c0 = r[4], c1 = r[5];
+        const f2 ww = pk(w, w);
+        upk(fma2(ww, pk(c0.x, c0.y), pk(a.c0, a.c1)), a.c0, a.c1);
+        upk(fma2(ww, pk(c0.z, c0.w), pk(a.c2, a.n0)), a.c2, a.n0);
+        upk(fma2(ww, pk(c1.x, c1.y), pk(a.n1, a.n2)), a.n1, a.n2);
     } else {
-        float4 c0, c1;
-        if (KIND == GS_PINHOLE) { c0 = r[4]; c1 = r[5]; } else { c0 = r[7]; c1 = r[8]; }
+        const float4 c0 = r[7], c1 = r[8];
         a.c0 = fmaf(w, c0.x, a.c0); a.c1 = fmaf(w, c0.y, a.c1); a.c2 = fmaf(w, c0.z, a.c2);
         a.n0 = fmaf(w, c0.w, a.n0); a.n1 = fmaf(w, c1.x, a.n1); a.n2 = fmaf(w, c1.y, a.n2);
     }
