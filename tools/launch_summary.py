@@ -3,7 +3,7 @@ of `bench.py --steps 1 --warmup 0 --timesteps T ...`: per kernel launches,
 total ms and share, over the timed step alone and over the whole command.
 
 The timed step is located as the T*7 frames that follow the instrumented
-planning pass (the last STATS compositor launch, template flag 1): each frame
+planning pass (the last STATS compositor launch, template flag STATS = 1): each frame
 starts with exactly one k_cull launch.
 
 python tools/launch_summary.py LAUNCHES.csv TIMESTEPS [title] > summary.md
@@ -51,7 +51,8 @@ def main():
     path, T = sys.argv[1], int(sys.argv[2])
     title = sys.argv[3] if len(sys.argv) > 3 else path
     rs = rows(path)
-    stats = [i for i, (_, k, _) in enumerate(rs) if re.search(r"k_render(_pinhole)?<(\d, )?1>", k)]
+    # the instrumented (STATS) compositor: k_render_pinhole<STATS, DEF>, k_render<KIND, STATS, DEF>
+    stats = [i for i, (_, k, _) in enumerate(rs) if re.search(r"k_render_pinhole<1, \d>|k_render<\d, 1, \d>", k)]
     start = stats[-1] + 1 if stats else 0
     culls = [i for i in range(start, len(rs)) if rs[i][1].startswith("k_cull")]
     nfr = 7 * T
