@@ -907,10 +907,21 @@ static bool is_default_ops(const DevOpts &o) {
            same(o.inv_sigma2, 1.0f / DEF_SIGMA2);
 }
 
-// Register budget (measured, tools/sweep.py): 64 registers per thread for
-// every sensor kind (six 5-warp CTAs per SM for the pinhole).
+// Register budgets (measured, tools/sweep.py): the pinhole compositor at 48
+// registers per thread (eight 5-warp CTAs per SM; 64 / 56 were 5-6 % slower
+// once the packed evaluation had lowered its pressure), fisheye and LiDAR at
+// 64.
+#ifndef GSR_PH_REGS
+#define GSR_PH_REGS 48
+#endif
+#ifndef GSR_RAY_REGS
+#define GSR_RAY_REGS 64
+#endif
+#ifndef GSR_RW_REGS
+#define GSR_RW_REGS 80   // the exact-stop re-walk of split lists
+#endif
 template <bool STATS, bool DEF>
-__global__ void __maxnreg__(64) k_render_pinhole(
+__global__ void __maxnreg__(GSR_PH_REGS) k_render_pinhole(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
@@ -922,7 +933,7 @@ __global__ void __maxnreg__(64) k_render_pinhole(
 }
 
 template <int KIND, bool STATS, bool DEF>
-__global__ void __maxnreg__(64) k_render(
+__global__ void __maxnreg__(GSR_RAY_REGS) k_render(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
@@ -1025,7 +1036,7 @@ __global__ void __launch_bounds__(512) k_merge_plan(
 // from each stopping sample's prefix transmittance; the segment's result is
 // added to the prefix composite and the sample written out.
 template <int KIND>
-__global__ void __maxnreg__(80) k_rewalk(
+__global__ void __maxnreg__(GSR_RW_REGS) k_rewalk(
     const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
     SchedHdr *h, const uint32_t *__restrict__ split_list, const float *__restrict__ mstate,
