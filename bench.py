@@ -295,7 +295,8 @@ def run_gsr(args):
     t_gen = time.time() - t_gen
 
     surf = to_device(surfels_np, device)
-    br = BatchRenderer(surf, device=device, n_streams=args.streams, grid_share=args.grid_share)
+    br = BatchRenderer(surf, device=device, n_streams=args.streams, grid_share=args.grid_share,
+                       priority=None if args.priority == "none" else args.priority)
     caps, contrib, evals = br.plan(my_sensors, stats=True)
     sensors = br.wrap(my_sensors)
 
@@ -322,7 +323,7 @@ def run_gsr(args):
                     on_frame(i, st)
                 if i % per_step_t != per_step_t - 1:
                     return
-                for lane_st in br.streams:
+                for lane_st in br.streams + [r for r in br.rstreams if r is not None]:
                     comm.wait_stream(lane_st)
                 with torch.cuda.stream(comm):
                     reqs.extend(sb.round(i // per_step_t))
@@ -566,7 +567,7 @@ def run_gsr(args):
 
     if rank == 0:
         desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
-                    if world > 1 else "1 GPU", streams=args.streams, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
+                    if world > 1 else "1 GPU", streams=args.streams, priority=args.priority, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
                     cuda_graph=graph_note,
                     l2="no flush: resident surfels (%.2f GB) and outputs (%.1f GB) exceed the 126 MB L2" % (
                         sum(v.numel() * 4 for v in surf.values() if isinstance(v, torch.Tensor)) / 1e9,
@@ -599,6 +600,9 @@ def main():
     ap.add_argument("--streams", type=int, default=10)
     ap.add_argument("--grid-share", type=float, default=None,
                     help="gs_opts.grid_share of every frame (default: BatchRenderer's 2/streams)")
+    ap.add_argument("--priority", choices=["none", "pre", "comp"], default="comp",
+                    help="per-lane stream priorities: projection + binning (pre) or compositing (comp) "
+                         "on a higher-priority stream; none: one stream per lane")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-frame rates")

@@ -27,9 +27,11 @@
 // (M^T h_u) x (M^T h_v) = det(M) M^{-1} (h_u x h_v): the kernels evaluate the
 // adjugate of the surfel map on the ray direction.  Records are written
 // relative to the surfel centre so that fp32 suffices here.
+#include <cuda.h>   // CUtensorMap (the TMA descriptor type; encoded through the runtime's driver entry point)
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "gsr_internal.cuh"
 
@@ -506,10 +508,37 @@ __device__ __forceinline__ void cp_async_arrive(void *b) {   // arrive when this
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
-__device__ __forceinline__ void pipe_init(Pipe &pp, int nw) {
+// TMA gather4 staging (sm_100a): the pinhole producer fills a 32-record slot
+// with eight cp.async.bulk.tensor.2d ... tile::gather4 copies (four 96-byte
+// record rows each, rows addressed by surfel id through a 2-D tensor map
+// over the record array) that complete on the slot's `full` mbarrier by
+// transaction count, instead of 192 16-byte cp.async ops.  The group
+// destinations (4 x 96 B) stay 128-byte aligned; the fisheye's 144-byte
+// records would not, so they keep cp.async.
+#ifndef GSR_TMA_GATHER
+#define GSR_TMA_GATHER 0   // 1: lanes 0-7 issue one gather4 each; 2: lane 0 issues all eight
+#endif
+#ifndef GSR_TMA_L2PROMO
+#define GSR_TMA_L2PROMO 1   // the tensor map's L2 promotion: 0 none, 1 128 B, 2 256 B
+#endif
+template <int KIND>
+constexpr bool TMA_STAGE = GSR_TMA_GATHER != 0 && KIND == GS_PINHOLE;
+__device__ __forceinline__ void mbar_arrive_expect_tx(void *b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, int r0, int r1, int r2, int r3,
+                                            void *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void pipe_init(Pipe &pp, int nw, uint32_t full_count) {
     if (threadIdx.x == 0) {
         for (int k = 0; k < KSLOTS; ++k) {
-            mbar_init(&pp.full[k], 32);   // the 32 producer lanes
+            mbar_init(&pp.full[k], full_count);   // the 32 producer lanes (cp.async) or one (TMA)
             mbar_init(&pp.empty[k], (uint32_t)nw);
             pp.stop_seq[k] = 0xffffffffu;
         }
@@ -572,7 +601,8 @@ __device__ __forceinline__ void eval_bits(uint32_t bits, const float4 *__restric
 // g: batches used so far by this CTA (the ring's phase clock, equal in all
 // threads).
 template <int KIND, bool STATS>
-__device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+__device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const CUtensorMap *tm,
+                                     const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *ring, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
                                      Acc &a, bool &done, bool &stopped, uint32_t &stop_b, Ckpt &ck,
@@ -599,11 +629,35 @@ __device__ __forceinline__ void walk_pipe(const float4 *__restrict__ rec, const 
             if (stop) {
                 if (lane == 0) pp.stop_seq[slot] = gg;
                 __syncwarp();
-                mbar_arrive(&pp.full[slot]);   // release: the STOP mark is visible to the waiters
+                if (!TMA_STAGE<KIND> || lane == 0)
+                    mbar_arrive(&pp.full[slot]);   // release: the STOP mark is visible to the waiters
                 used = b + 1;
                 break;
             }
             const uint32_t first = s + b * 32;
+            if constexpr (TMA_STAGE<KIND>) {
+                // lane q < 8 gathers records 4q..4q+3 of the batch (a short last batch
+                // repeats its last record; consumers ignore lanes >= cnt)
+                const uint32_t id = __ldg(values + min(first + lane, e - 1));
+                if (GSR_TMA_GATHER == 2) {   // lane 0 issues all eight
+                    if (lane == 0) mbar_arrive_expect_tx(&pp.full[slot], 32u * R4 * 16u);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int r0 = (int)__shfl_sync(FULL, id, 4 * q), r1 = (int)__shfl_sync(FULL, id, 4 * q + 1);
+                        const int r2 = (int)__shfl_sync(FULL, id, 4 * q + 2), r3 = (int)__shfl_sync(FULL, id, 4 * q + 3);
+                        if (lane == 0) tma_gather4(ring + (slot * 32 + 4 * q) * S4, tm, r0, r1, r2, r3, &pp.full[slot]);
+                    }
+                    continue;
+                }
+                const int q4 = (lane & 7) * 4;
+                const int r0 = (int)__shfl_sync(FULL, id, q4), r1 = (int)__shfl_sync(FULL, id, q4 + 1);
+                const int r2 = (int)__shfl_sync(FULL, id, q4 + 2), r3 = (int)__shfl_sync(FULL, id, q4 + 3);
+                if (lane == 0) mbar_arrive_expect_tx(&pp.full[slot], 32u * R4 * 16u);
+                __syncwarp();
+                if (lane < 8)
+                    tma_gather4(ring + (slot * 32 + q4) * S4, tm, r0, r1, r2, r3, &pp.full[slot]);
+                continue;
+            }
             if (first + lane < e) {
                 const uint32_t id = __ldg(values + first + lane);
                 const float4 *src = rec + (size_t)id * R4;
@@ -700,13 +754,14 @@ __device__ __forceinline__ void walk_self(const float4 *__restrict__ rec, const 
 }
 
 template <int KIND, bool STATS>
-__device__ __forceinline__ void walk(bool piped, const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+__device__ __forceinline__ void walk(bool piped, const float4 *__restrict__ rec, const CUtensorMap *tm,
+                                     const uint32_t *__restrict__ values,
                                      uint32_t s, uint32_t e, float4 *smem, Pipe &pp, uint32_t &g,
                                      const SubTile &st, const Ray &ry, const DevSensor &se, const DevOpts &op,
                                      Acc &a, bool &done, bool &stopped, uint32_t &stop_b, Ckpt &ck,
                                      uint32_t &n_eval, uint32_t &n_comp) {
     if (piped)
-        walk_pipe<KIND, STATS>(rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
+        walk_pipe<KIND, STATS>(rec, tm, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
                                n_eval, n_comp);
     else
         walk_self<KIND, STATS>(rec, values, s, e, smem, st, ry, se, op, a, done, stopped, stop_b, ck, n_eval,
@@ -826,7 +881,7 @@ __global__ void k_sched_fill(const uint2 *__restrict__ ranges, int ntiles, const
 // their local composite (T = 1 at the segment start) in `partials` (SoA).
 template <int KIND, bool STATS>
 __device__ __forceinline__ void render_body(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const float4 *__restrict__ rec, const CUtensorMap *tm, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const DevSensor &se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
@@ -834,7 +889,7 @@ __device__ __forceinline__ void render_body(
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
     const uint32_t L = seg_len(h, lfix, ctas);
     const uint32_t cb = ckpt_batches(L);
-    extern __shared__ float4 smem[];
+    extern __shared__ __align__(128) float4 smem[];   // TMA destinations: 128-byte aligned
     __shared__ uint32_t s_item;
     __shared__ Pipe pp;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -843,7 +898,7 @@ __device__ __forceinline__ void render_body(
     const bool cons = warp < nw;
     const bool ovf = frame_ovf(d_overflow, h);
     const uint32_t n_items = h->n_items;
-    if (piped) pipe_init(pp, nw);
+    if (piped) pipe_init(pp, nw, TMA_STAGE<KIND> ? 1u : 32u);
     uint32_t g = 0;
     while (true) {
         if (t == 0) s_item = atomicAdd(&h->counter, 1u);
@@ -865,7 +920,7 @@ __device__ __forceinline__ void render_body(
         uint32_t n_eval = 0, n_comp = 0, stop_b = NO_STOP;
         Ckpt ck = make_ckpt(ns > 1 && cons ? ckpt + (size_t)(split_base[tile] + seg) * NCP * NPART * npix : nullptr,
                             cb, npix, t);
-        walk<KIND, STATS>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
+        walk<KIND, STATS>(piped, rec, tm, values, s, e, smem, pp, g, st, ry, se, op, a, done, stopped, stop_b, ck,
                           n_eval, n_comp);
         if (!cons) continue;
         if (ns == 1) {
@@ -922,25 +977,25 @@ static bool is_default_ops(const DevOpts &o) {
 #endif
 template <bool STATS, bool DEF>
 __global__ void __maxnreg__(GSR_PH_REGS) k_render_pinhole(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const float4 *__restrict__ rec, const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
-    render_body<GS_PINHOLE, STATS>(rec, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
+    render_body<GS_PINHOLE, STATS>(rec, &tmap, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
                                    partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
 }
 
 template <int KIND, bool STATS, bool DEF>
 __global__ void __maxnreg__(GSR_RAY_REGS) k_render(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const float4 *__restrict__ rec, const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const int32_t *__restrict__ d_overflow,
     const __grid_constant__ DevSensor se, const DevOpts op, SchedHdr *h,
     const uint2 *__restrict__ items, const uint32_t *__restrict__ split_base,
     float *__restrict__ partials, float *__restrict__ ckpt, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t *__restrict__ out_stats, uint32_t lfix, uint32_t ctas) {
-    render_body<KIND, STATS>(rec, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
+    render_body<KIND, STATS>(rec, &tmap, values, ranges, d_overflow, se, DEF ? default_ops(op) : op, h, items, split_base,
                              partials, ckpt, o0, o1, o2, o3, out_stats, lfix, ctas);
 }
 
@@ -1037,14 +1092,14 @@ __global__ void __launch_bounds__(512) k_merge_plan(
 // added to the prefix composite and the sample written out.
 template <int KIND>
 __global__ void __maxnreg__(GSR_RW_REGS) k_rewalk(
-    const float4 *__restrict__ rec, const uint32_t *__restrict__ values,
+    const float4 *__restrict__ rec, const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ values,
     const uint2 *__restrict__ ranges, const __grid_constant__ DevSensor se, const DevOpts op,
     SchedHdr *h, const uint32_t *__restrict__ split_list, const float *__restrict__ mstate,
     const uint2 *__restrict__ rw_items, float *__restrict__ o0, float *__restrict__ o1,
     float *__restrict__ o2, float *__restrict__ o3, uint32_t lfix, uint32_t ctas) {
     const uint32_t L = seg_len(h, lfix, ctas);
     const uint32_t cb = ckpt_batches(L);
-    extern __shared__ float4 smem[];
+    extern __shared__ __align__(128) float4 smem[];   // TMA destinations: 128-byte aligned
     __shared__ uint32_t s_item;
     __shared__ Pipe pp;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -1052,7 +1107,8 @@ __global__ void __maxnreg__(GSR_RW_REGS) k_rewalk(
     const int nw = piped ? (int)(blockDim.x >> 5) - 1 : 1, npix = nw * 32;
     const bool cons = warp < nw;
     const uint32_t n_items = h->rw_count;
-    if (piped) pipe_init(pp, nw);
+    const CUtensorMap *tm = &tmap;
+    if (piped) pipe_init(pp, nw, TMA_STAGE<KIND> ? 1u : 32u);
     uint32_t g = 0;
     while (true) {
         if (t == 0) s_item = atomicAdd(&h->rw_counter, 1u);
@@ -1075,7 +1131,7 @@ __global__ void __maxnreg__(GSR_RW_REGS) k_rewalk(
         // the chunk between checkpoints c and c+1 of segment k (the ray stops inside it)
         const uint32_t seg_s = rg.x + k * L, seg_e = min(rg.y, seg_s + L);
         const uint32_t s = min(seg_e, seg_s + c * cb * 32u), e = min(seg_e, seg_s + (c + 1u) * cb * 32u);
-        walk<KIND, false>(piped, rec, values, s, e, smem, pp, g, st, ry, se, op, r, done, stopped, sb, ck, ne, nc);
+        walk<KIND, false>(piped, rec, tm, values, s, e, smem, pp, g, st, ry, se, op, r, done, stopped, sb, ck, ne, nc);
         if (mine) {
             Acc a = {r.T, m[1 * npix] + r.A, m[2 * npix] + r.c0, m[3 * npix] + r.c1, m[4 * npix] + r.c2,
                      m[5 * npix] + r.d, m[6 * npix] + r.n0, m[7 * npix] + r.n1, m[8 * npix] + r.n2};
@@ -1085,6 +1141,37 @@ __global__ void __maxnreg__(GSR_RW_REGS) k_rewalk(
 }
 
 // ---------------------------------------------------------------- host
+// The record array as a 2-D fp32 tensor [n rows][F columns] for the gather4
+// staging: box = one full row, no swizzle / interleave, row stride F*4 bytes.
+// cuTensorMapEncodeTiled is reached through the runtime's driver entry point
+// (no link against libcuda); the descriptor travels as a __grid_constant__
+// kernel parameter, so it is captured with the launch in a CUDA graph.
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                     CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                     CUtensorMapFloatOOBfill);
+static cudaError_t record_tmap(CUtensorMap *m, const float4 *rec, int64_t n, int F) {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    });
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {(cuuint64_t)F, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)F * 4u};
+    const cuuint32_t box[2] = {(cuuint32_t)F, 1u}, estr[2] = {1u, 1u};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)rec, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          GSR_TMA_L2PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                          : GSR_TMA_L2PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 size_t render_workspace_bytes(int64_t cap, int64_t ntiles, int32_t split_len, int npix) {
     return RenderWs(cap, ntiles, split_len, npix).total;
 }
@@ -1098,6 +1185,12 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     const float4 *rec = (const float4 *)((const char *)proj + PL.rec);
     const int ntiles = se.ntx * se.nty;
     const int npix = se.tw * se.th;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (TMA_STAGE<KIND> && npix > 32 && n > 0) {
+        cudaError_t te = record_tmap(&tmap, rec, n, Rec<KIND>::F);
+        if (te != cudaSuccess) return te;
+    }
     // capacity implied by the workspace size (the pair capacity of gs_bin_sort)
     int64_t cap = 0;
     {
@@ -1143,7 +1236,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
-    kern<<<grid, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, d_overflow, se, op, h,
+    kern<<<grid, nthr, sm, st>>>(rec, tmap, values, (const uint2 *)ranges, d_overflow, se, op, h,
                                                   items, split_base, partials, ckpt, o0, o1, o2, o3, stats, lfix,
                                                   ctas);
     e = cudaGetLastError();
@@ -1160,7 +1253,7 @@ static cudaError_t launch(const void *proj, int64_t n, const uint32_t *values, c
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_rw, k_rewalk<KIND>, nthr, sm);
         const unsigned grid_rw = (unsigned)std::max<int64_t>(
             1, std::min<int64_t>((int64_t)((float)(nsm * std::max(per_rw, 1)) * op.grid_share), (int64_t)W.max_slots));
-        k_rewalk<KIND><<<grid_rw, nthr, sm, st>>>(rec, values, (const uint2 *)ranges, se, op, h, split_list,
+        k_rewalk<KIND><<<grid_rw, nthr, sm, st>>>(rec, tmap, values, (const uint2 *)ranges, se, op, h, split_list,
                                                   mstate, rw_items, o0, o1, o2, o3, lfix, ctas);
         e = cudaGetLastError();
     }

@@ -24,7 +24,10 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;   // 4096
 constexpr int RS_BINS = 256;
-constexpr int RS_LB = 8;   // look-back window: predecessor tiles read per round trip
+#ifndef GSR_RS_LB
+#define GSR_RS_LB 8
+#endif
+constexpr int RS_LB = GSR_RS_LB;   // look-back window: predecessor tiles read per round trip
 constexpr uint32_t RS_AGG = 1u << 30, RS_PRE = 2u << 30, RS_VAL = (1u << 30) - 1;
 
 struct SortWs {   // workspace layout of gs_bin_sort
@@ -178,34 +181,11 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
         whist[w][dg] = cnt;
         cnt += c;
     }
-    // decoupled look-back over tiles for this digit
-    uint32_t excl = 0;
+    // decoupled look-back over tiles for this digit: post this tile's count now;
+    // the look-back itself runs after the keys are staged in shared memory
+    // (their registers are free then for a wide window of predecessor reads)
     uint32_t *st = status + (size_t)tile * RS_BINS + dg;
-    if (tile == 0) {
-        st_volatile_u32(st, RS_PRE | cnt);
-    } else {
-        st_volatile_u32(st, RS_AGG | cnt);
-        // look back RS_LB predecessors per round trip (independent loads), consuming
-        // them in order until an inclusive prefix; an unposted one is re-read
-        int64_t t = (int64_t)tile - 1;
-        bool done = false;
-        while (!done) {
-            uint32_t sv[RS_LB];
-#pragma unroll
-            for (int q = 0; q < RS_LB; ++q)
-                sv[q] = t - q >= 0 ? ld_volatile_u32(status + (size_t)(t - q) * RS_BINS + dg) : RS_PRE;
-            int q = 0;
-            for (; q < RS_LB; ++q) {
-                const uint32_t f = sv[q] >> 30;
-                if (f == 0) break;
-                excl += sv[q] & RS_VAL;
-                if (f == 2) { done = true; break; }
-            }
-            t -= q;
-        }
-        st_volatile_u32(st, RS_PRE | (excl + cnt));
-    }
-    glob[dg] = gbase[dg] + excl;
+    st_volatile_u32(st, (tile == 0 ? RS_PRE : RS_AGG) | cnt);
     // tile-local exclusive scan over digits (block scan of cnt)
     {
         uint32_t x = warp_inclusive_scan<uint32_t>(cnt);
@@ -230,6 +210,34 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_onesweep(
             skey[pos] = k[j];
             sval[pos] = v[j];
         }
+    }
+    {
+        // look back RS_LB predecessors per round trip (independent loads), consuming
+        // them in order until an inclusive prefix; an unposted one is re-read.  In
+        // the first wave every tile starts at once, so tile t walks ~t / RS_LB round
+        // trips before it meets an inclusive prefix: the window sets that chain.
+        uint32_t excl = 0;
+        if (tile > 0) {
+            int64_t t = (int64_t)tile - 1;
+            bool done = false;
+            while (!done) {
+                uint32_t sv[RS_LB];
+#pragma unroll
+                for (int q = 0; q < RS_LB; ++q)
+                    sv[q] = t - q >= 0 ? ld_volatile_u32(status + (size_t)(t - q) * RS_BINS + dg) : RS_PRE;
+                int q = 0;
+#pragma unroll
+                for (; q < RS_LB; ++q) {
+                    const uint32_t f = sv[q] >> 30;
+                    if (f == 0) break;
+                    excl += sv[q] & RS_VAL;
+                    if (f == 2) { done = true; break; }
+                }
+                t -= q;
+            }
+            st_volatile_u32(st, RS_PRE | (excl + cnt));
+        }
+        glob[dg] = gbase[dg] + excl;
     }
     __syncthreads();
     const uint32_t nt = min((uint32_t)RS_TILE, n - t0);

@@ -84,7 +84,7 @@ class Renderer:
     def render(self, sensor, out: torch.Tensor | None = None, capacity: int | None = None,
                keys: bool = False, stream=None, stats: torch.Tensor | None = None,
                events=None, overflow: torch.Tensor | None = None,
-               opts: gsr.gs_opts | None = None) -> torch.Tensor:
+               opts: gsr.gs_opts | None = None, render_stream=None) -> torch.Tensor:
         """Render one frame; returns a planar fp32 tensor [C,H,W] (C = 8 for
         cameras: r,g,b,depth,nx,ny,nz,alpha; 4 for LiDAR: range, intensity,
         raydrop, alpha).  stats: optional int32 [2,H,W] (composited, evaluated
@@ -92,7 +92,9 @@ class Renderer:
         gs_project, gs_bin_sort, the render call and after it.  overflow:
         optional int32 device slot for gs_bin_sort's overflow flag (default:
         a buffer owned by the renderer).  opts: this frame's options instead
-        of the renderer's (e.g. another tile shape)."""
+        of the renderer's (e.g. another tile shape).  render_stream: a torch
+        stream the render call runs on after gs_bin_sort (event-ordered), e.g. one
+        of another priority; default: the current stream."""
         if not isinstance(sensor, gsr.Sensor):
             sensor = gsr.Sensor(sensor)
         self.opts = self.opts_for(sensor)
@@ -120,6 +122,10 @@ class Renderer:
         if out is None:
             out = torch.empty((C, H, W), dtype=torch.float32, device=self.device)
         rws = self._get("rws", gsr.gs_render_workspace_bytes(cap, sensor, self.opts))
+        if render_stream is not None:
+            render_stream.wait_stream(torch_stream)
+            torch_stream = render_stream
+            st = render_stream.cuda_stream
         if events is not None:
             events[2].record(torch_stream)
         if sensor.kind == gsr.GS_LIDAR_SPINNING:
