@@ -279,7 +279,7 @@ def run_gsr(args):
     from paper_2503_11731_b200 import dist as gd
     from paper_2503_11731_b200 import gsr
     from paper_2503_11731_b200.batch import BatchRenderer, FrameTimes
-    from paper_2503_11731_b200.render import to_device
+    from paper_2503_11731_b200.render import cull_bounds, to_device
 
     rank, world, device = gd.init()
     if device.type != "cuda":
@@ -465,7 +465,8 @@ def run_gsr(args):
     # ---------------- end to end: host buffers through the public API
     e2e = None
     if not args.no_e2e:
-        host = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in surf.items()}
+        host = {k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in surf.items()
+                if k != "cull_bounds"}
         h2d = sum(v.numel() * v.element_size() for v in host.values() if isinstance(v, torch.Tensor))
         # rank 0 receives the whole gathered batch into pinned host memory
         host_src = slabs_full if rank == 0 else {}
@@ -505,7 +506,7 @@ def run_gsr(args):
                 if used[bi] is not None:
                     up_stream.wait_event(used[bi])   # that copy's previous renders are done
                 for k, v in host.items():
-                    if isinstance(v, torch.Tensor):
+                    if isinstance(v, torch.Tensor) and k != "cull_bounds":
                         dev2[bi][k].copy_(v, non_blocking=True)
                 up_done[bi] = torch.cuda.Event()
                 up_done[bi].record(up_stream)
@@ -515,6 +516,12 @@ def run_gsr(args):
             if j == 0:
                 upload(0)
             cur.wait_event(up_done[bi])
+            # the block bounds of the hierarchical cull are recomputed on the device from the
+            # uploaded surfels (gs_cull_bounds), inside the timed region like the copy; on the
+            # rendering stream: a kernel queued behind the upload stream's copies would hold up
+            # whichever lanes share its hardware queue until the copies finish
+            if dev2[bi].get("cull_bounds") is not None:
+                cull_bounds(dev2[bi])
             if not last:
                 upload(j + 1)
             if graphs2[bi] is not None:

@@ -91,7 +91,26 @@ typedef struct {
     int32_t sh_degree;           /* d in 0..3                                           */
     const float *intensity;      /* [n] LiDAR intensity r in [0,1]; LiDAR only          */
     const float *raydrop_logit;  /* [n] LiDAR ray-drop logit (p = sigmoid); LiDAR only  */
+    const float *cull_bounds;    /* optional (NULL = none): gs_cull_bounds' output for
+                                    exactly these means / scales, see below            */
 } gs_surfels;
+
+/* Block bounds for a hierarchical frustum cull (the paper renders from
+ * per-zone resident sets, §III-A "Support Large-scale Scenes";
+ * here every block of GS_CULL_BLOCK consecutive surfels carries a bound, so a
+ * scene stored zone by zone is culled zone by zone without the renderer
+ * knowing the zones).  bounds: device, [gs_cull_blocks(n)][8] fp32 =
+ * min x,y,z and max x,y,z of the block's finite centres, the block's largest
+ * finite scale, 0.  gs_project with surfels->cull_bounds set skips (pinhole
+ * sensors) the per-surfel cull of a block that lies wholly outside the
+ * frustum or in front of the near plane; its outputs are bitwise those
+ * without bounds -- a skipped block holds only surfels the per-surfel cull
+ * drops (tests/test_gpu_dims.py).  The bounds describe the arrays they were
+ * computed from: recompute after any change of means or scales (one pass,
+ * 20 bytes read per surfel; asynchronous on `stream`). */
+#define GS_CULL_BLOCK 2048
+int64_t gs_cull_blocks(int64_t n);
+gs_status gs_cull_bounds(const gs_surfels *surfels, float *bounds, gs_stream stream);
 
 /* Sensor model.  world_to_sensor = [R|t] row-major 3x4:
  * p_sensor = R p_world + t.  Camera frame x right, y down, z forward; LiDAR

@@ -10,6 +10,7 @@
 #include "gsr_internal.cuh"
 
 namespace gsr {
+cudaError_t launch_bounds(const DevSurfels &, float *, cudaStream_t);
 cudaError_t launch_project(const DevSurfels &, const DevSensor &, const DevOpts &, void *, int64_t *,
                            cudaStream_t);
 size_t sort_workspace_bytes(int64_t n, int64_t cap, int64_t ntiles);
@@ -272,11 +273,29 @@ extern "C" gs_status gs_project(const gs_surfels *sf, const gs_sensor *s, const 
     ds.means = sf->means; ds.quats = sf->quats; ds.scales = sf->scales; ds.opac = sf->opacities;
     ds.sh = sf->sh; ds.inten = sf->intensity; ds.drop = sf->raydrop_logit;
     ds.sh_degree = sf->sh_degree;
+    ds.bounds = sf->cull_bounds;
+    if (ds.bounds && ((uintptr_t)ds.bounds & 15) != 0) return fail(GS_ERR_CONFIG, "cull_bounds must be 16-byte aligned");
     const DevSensor se = make_dev_sensor(s, o);
     const DevOpts op = make_dev_opts(o);
     cudaError_t e = launch_project(ds, se, op, projected, d_num_pairs, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gs_project");
     return GS_OK;
+}
+
+extern "C" int64_t gs_cull_blocks(int64_t n) { return n > 0 ? (n + SCAN_TILE - 1) / SCAN_TILE : 0; }
+static_assert(GS_CULL_BLOCK == SCAN_TILE, "gsr.h block size");
+
+extern "C" gs_status gs_cull_bounds(const gs_surfels *sf, float *bounds, gs_stream stream) {
+    if (!sf) return fail(GS_ERR_CONFIG, "surfels is NULL");
+    if (sf->n < 0 || sf->n >= (1ll << 30)) return fail(GS_ERR_RANGE, "surfel count outside [0, 2^30)");
+    if (sf->n == 0) return GS_OK;
+    if (!sf->means || !sf->scales || !bounds) return fail(GS_ERR_CONFIG, "null pointer");
+    if (((uintptr_t)sf->scales & 7) != 0) return fail(GS_ERR_CONFIG, "scales must be 8-byte aligned");
+    if (((uintptr_t)bounds & 15) != 0) return fail(GS_ERR_CONFIG, "bounds must be 16-byte aligned");
+    DevSurfels ds{};
+    ds.n = sf->n; ds.means = sf->means; ds.scales = sf->scales;
+    const cudaError_t e = launch_bounds(ds, bounds, (cudaStream_t)stream);
+    return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_cull_bounds");
 }
 
 extern "C" gs_status gs_bin_sort(const void *projected, int64_t n, const gs_sensor *s, const gs_opts *o,
@@ -426,6 +445,7 @@ extern "C" gs_status gs_pack_surfels(const gs_surfels *src, const uint32_t *d_in
     DevSurfels d;
     d.n = src->n; d.means = src->means; d.quats = src->quats; d.scales = src->scales; d.opac = src->opacities;
     d.sh = src->sh; d.sh_degree = src->sh_degree; d.inten = src->intensity; d.drop = src->raydrop_logit;
+    d.bounds = nullptr;
     const int nsh = src->sh ? (src->sh_degree + 1) * (src->sh_degree + 1) * 3 : 0;
     const cudaError_t e = launch_pack(d, nsh, d_index, m, payload, (cudaStream_t)stream);
     return e == cudaSuccess ? GS_OK : cuda_fail(e, "gs_pack_surfels");
@@ -473,6 +493,7 @@ extern "C" gs_status gs_render_backward(const gs_surfels *sf, const gs_sensor *s
     ds.means = sf->means; ds.quats = sf->quats; ds.scales = sf->scales; ds.opac = sf->opacities;
     ds.sh = sf->sh; ds.inten = sf->intensity; ds.drop = sf->raydrop_logit;
     ds.sh_degree = sf->sh_degree;
+    ds.bounds = nullptr;
     const DevSensor se = make_dev_sensor(s, o);
     const DevOpts op = make_dev_opts(o);
     const cudaError_t e = launch_backward(ds, se, op, projected, values, tile_ranges, grad_out, workspace, d_means,

@@ -39,6 +39,7 @@ struct DevSurfels {
     int64_t n;
     const float *means, *quats, *scales, *opac, *sh, *inten, *drop;
     int32_t sh_degree;
+    const float *bounds;   // optional block bounds (gs_cull_bounds), [n / SCAN_TILE][8]
 };
 
 // ---------------------------------------------------------------- records

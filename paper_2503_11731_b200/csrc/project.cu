@@ -451,6 +451,96 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
     return lo < se.nbeams && sb[lo] >= sl;
 }
 
+// Block bounds (gs_cull_bounds): min / max of the finite centres and the
+// largest finite scale of every SCAN_TILE consecutive surfels.  fminf / fmaxf
+// drop NaNs; an infinite centre gives an infinite bound, which block_outside
+// never rejects; a surfel with a NaN centre or a non-finite scale fails
+// cull_one whatever its block says.
+__global__ void __launch_bounds__(SCAN_THREADS) k_bounds(const float *__restrict__ means,
+                                                         const float *__restrict__ scales, int64_t n,
+                                                         float *__restrict__ bounds) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, sm = 0.f;
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
+        if (i < n) {
+            for (int k = 0; k < 3; ++k) {
+                const float m = __ldg(means + 3 * i + k);
+                lo[k] = fminf(lo[k], m);
+                hi[k] = fmaxf(hi[k], m);
+            }
+            const float2 sc = __ldg(reinterpret_cast<const float2 *>(scales) + i);
+            if (isfinite(sc.x)) sm = fmaxf(sm, sc.x);
+            if (isfinite(sc.y)) sm = fmaxf(sm, sc.y);
+        }
+    }
+    __shared__ float red[SCAN_THREADS / 32][7];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = 16; o; o >>= 1) {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = fminf(lo[k], __shfl_xor_sync(FULL_MASK, lo[k], o));
+            hi[k] = fmaxf(hi[k], __shfl_xor_sync(FULL_MASK, hi[k], o));
+        }
+        sm = fmaxf(sm, __shfl_xor_sync(FULL_MASK, sm, o));
+    }
+    if (lane == 0) {
+        for (int k = 0; k < 3; ++k) { red[warp][k] = lo[k]; red[warp][3 + k] = hi[k]; }
+        red[warp][6] = sm;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < SCAN_THREADS / 32; ++w) {
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = fminf(lo[k], red[w][k]);
+                hi[k] = fmaxf(hi[k], red[w][3 + k]);
+            }
+            sm = fmaxf(sm, red[w][6]);
+        }
+        float *b = bounds + (size_t)blockIdx.x * 8;
+        b[0] = lo[0]; b[1] = lo[1]; b[2] = lo[2]; b[3] = hi[0]; b[4] = hi[1]; b[5] = hi[2];
+        b[6] = sm; b[7] = 0.f;
+    }
+}
+
+// True when every surfel of the block fails cull_one<GS_PINHOLE>: the block's
+// box of centres, widened by the largest support sphere of the block, lies
+// behind the near plane or outside one frustum side.  Each test bounds the
+// quantity cull_one compares (a linear function of the centre: centre value
+// plus the box half-extents times the absolute coefficients) and rejects only
+// with twice cull_one's own fp32 margin to spare; every comparison is false
+// on a NaN, so a block with non-finite bounds is never rejected.
+__device__ __forceinline__ bool block_outside(const float *__restrict__ bnd, const DevSensor &se,
+                                              const DevOpts &op) {
+    const float4 b0 = __ldg(reinterpret_cast<const float4 *>(bnd)), b1 = __ldg(reinterpret_cast<const float4 *>(bnd) + 1);
+    const float c[3] = {0.5f * (b0.x + b0.w), 0.5f * (b0.y + b1.x), 0.5f * (b0.z + b1.y)};
+    // half extents, rounded up (the centre above is rounded too)
+    const float h[3] = {(b0.w - b0.x) * 0.5000005f + 1e-6f * fabsf(c[0]), (b1.x - b0.y) * 0.5000005f + 1e-6f * fabsf(c[1]),
+                        (b1.y - b0.z) * 0.5000005f + 1e-6f * fabsf(c[2])};
+    if (!(h[0] >= 0.f) || !(h[1] >= 0.f) || !(h[2] >= 0.f)) return false;   // empty or non-finite block
+    float Xc[3], Xe[3];
+    for (int r = 0; r < 3; ++r) {
+        Xc[r] = fmaf(se.R[3 * r], c[0], fmaf(se.R[3 * r + 1], c[1], fmaf(se.R[3 * r + 2], c[2], se.t[r])));
+        Xe[r] = fabsf(se.R[3 * r]) * h[0] + fabsf(se.R[3 * r + 1]) * h[1] + fabsf(se.R[3 * r + 2]) * h[2];
+    }
+    // magnitude bound of any centre of the block in both frames (cull_one's margins scale with it)
+    const float magw = fabsf(c[0]) + h[0] + fabsf(c[1]) + h[1] + fabsf(c[2]) + h[2] + fabsf(se.t[0]) + fabsf(se.t[1]) +
+                       fabsf(se.t[2]);
+    const float mags = fabsf(Xc[0]) + Xe[0] + fabsf(Xc[1]) + Xe[1] + fabsf(Xc[2]) + Xe[2];
+    const float slack = 3e-3f * (1.f + mags) + 3e-5f * magw;   // > 2x cull_one's margins + this function's rounding
+    // near plane: cull_one drops Z < near - (1e-5 mag + 1e-6)
+    if (Xc[2] + Xe[2] < op.near_plane - slack) return true;
+    const float R = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f) * b1.z + slack;   // >= every surfel's R
+    const float m = 1.f + sqrtf(op.support * 1.0001f + 1e-4f) * sqrtf(op.sigma2);
+    const float xl = (-m - se.cx) / se.fx, xr = ((float)se.width + m - se.cx) / se.fx;
+    const float yl = (-m - se.cy) / se.fy, yr = ((float)se.height + m - se.cy) / se.fy;
+    // f(X) = a X + b Y + g Z over the block: f(Xc) + |a| Xe_x + |b| Xe_y + |g| Xe_z
+    if ((Xc[0] - xl * Xc[2]) + Xe[0] + fabsf(xl) * Xe[2] < -R * sqrtf(1.f + xl * xl) - slack) return true;
+    if ((xr * Xc[2] - Xc[0]) + Xe[0] + fabsf(xr) * Xe[2] < -R * sqrtf(1.f + xr * xr) - slack) return true;
+    if ((Xc[1] - yl * Xc[2]) + Xe[1] + fabsf(yl) * Xe[2] < -R * sqrtf(1.f + yl * yl) - slack) return true;
+    if ((yr * Xc[2] - Xc[1]) + Xe[1] + fabsf(yr) * Xe[2] < -R * sqrtf(1.f + yr * yr) - slack) return true;
+    return false;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __grid_constant__ DevSensor se,
                                                        DevOpts op, short4 *__restrict__ rect,
@@ -469,12 +559,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
     // item j of thread t: base + j * SCAN_THREADS + t (coalesced); ranks in index order via per-round ballots
     const int64_t base = (int64_t)tile * SCAN_TILE;
     uint32_t flags = 0, cnt = 0;
+    // hierarchical cull: a block wholly outside the frustum skips the per-surfel pass
+    // (its surfels still get their zero counts and the tile its place in the look-back)
+    const bool skip = KIND == GS_PINHOLE && s.bounds && block_outside(s.bounds + (size_t)tile * 8, se, op);
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
         if (i < s.n) {
             uint32_t kb;
-            const bool c = cull_one<KIND>(s, se, op, i, kb, sb);
+            const bool c = !skip && cull_one<KIND>(s, se, op, i, kb, sb);
             if (c) { flags |= 1u << j; ++cnt; }
             // every surfel gets a zero pair count here (coalesced); k_project writes
             // count, key and rect of every candidate.  Nothing reads the key or rect
@@ -1148,6 +1241,14 @@ cudaError_t launch_project(const DevSurfels &s, const DevSensor &se, const DevOp
     }
     k_compact<<<nblk, SCAN_THREADS, 0, st>>>(key, cnt, cand, s.n, (uint32_t *)(base + L.vkey), (uint32_t *)(base + L.vid),
                                             stv, stp, hdr, d_num_pairs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bounds(const DevSurfels &s, float *bounds, cudaStream_t st) {
+    if (s.n == 0) return cudaSuccess;
+    const unsigned nblk = (unsigned)((s.n + SCAN_TILE - 1) / SCAN_TILE);
+    note_launch();
+    k_bounds<<<nblk, SCAN_THREADS, 0, st>>>(s.means, s.scales, s.n, bounds);
     return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ class gs_surfels(C.Structure):
     _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("quats", C.c_void_p),
                 ("scales", C.c_void_p), ("opacities", C.c_void_p), ("sh", C.c_void_p),
                 ("sh_degree", C.c_int32), ("intensity", C.c_void_p),
-                ("raydrop_logit", C.c_void_p)]
+                ("raydrop_logit", C.c_void_p), ("cull_bounds", C.c_void_p)]
 
 
 class gs_sensor(C.Structure):
@@ -73,7 +73,7 @@ EXPORTS = ["gs_default_opts", "gs_decode_anchors", "gs_backward_workspace_bytes"
            "gs_payload_floats", "gs_pack_surfels", "gs_unpack_surfels", "gs_projected_bytes", "gs_sort_workspace_bytes", "gs_num_tiles", "gs_projected_offsets",
            "gs_project", "gs_bin_sort", "gs_render_camera", "gs_render_lidar",
            "gs_status_string", "gs_last_error", "gs_record_bytes", "gs_render_workspace_bytes",
-           "gs_kernel_launches"]
+           "gs_kernel_launches", "gs_cull_blocks", "gs_cull_bounds"]
 
 _lib = None
 
@@ -138,6 +138,10 @@ def load(build_if_missing: bool = True):
     lib.gs_render_backward.argtypes = [P(gs_surfels), P(gs_sensor), P(gs_opts), vp, vp, vp, vp, vp, C.c_size_t,
                                        vp, vp, vp, vp, vp, vp, vp, vp]
     lib.gs_render_backward.restype = C.c_int
+    lib.gs_cull_blocks.argtypes = [C.c_int64]
+    lib.gs_cull_blocks.restype = C.c_int64
+    lib.gs_cull_bounds.argtypes = [P(gs_surfels), vp, vp]
+    lib.gs_cull_bounds.restype = C.c_int
     lib.gs_kernel_launches.argtypes = []
     lib.gs_kernel_launches.restype = C.c_uint64
     _lib = lib
@@ -201,7 +205,16 @@ def surfels_struct(t: dict) -> gs_surfels:
     s.sh_degree = int(t.get("sh_degree", 0))
     s.intensity = t["intensity"].data_ptr() if t.get("intensity") is not None else None
     s.raydrop_logit = t["raydrop_logit"].data_ptr() if t.get("raydrop_logit") is not None else None
+    s.cull_bounds = t["cull_bounds"].data_ptr() if t.get("cull_bounds") is not None else None
     return s
+
+
+def gs_cull_blocks(n):
+    return int(load().gs_cull_blocks(int(n)))
+
+
+def gs_cull_bounds(surfels: gs_surfels, bounds, stream):
+    _check(load().gs_cull_bounds(C.byref(surfels), _ptr(bounds), stream))
 
 
 # ---------------------------------------------------------------- the C-ABI, same names

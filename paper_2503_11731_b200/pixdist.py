@@ -99,7 +99,9 @@ def shard_surfels(surfels: dict, world: int, rank: int) -> dict:
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)
     hi = lo + base + (1 if rank < extra else 0)
-    return {k: (v[lo:hi] if isinstance(v, torch.Tensor) else v) for k, v in surfels.items()}
+    # the whole set's block bounds do not describe a shard: the shard renders without
+    # (render.cull_bounds(shard) would give it its own)
+    return {k: (v[lo:hi] if isinstance(v, torch.Tensor) else v) for k, v in surfels.items() if k != "cull_bounds"}
 
 
 # ---------------------------------------------------------------- per-rank steps (device)

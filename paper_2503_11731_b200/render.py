@@ -22,12 +22,34 @@ CAMERA_CHANNELS = ("r", "g", "b", "depth", "nx", "ny", "nz", "alpha")
 LIDAR_CHANNELS = ("range", "intensity", "raydrop", "alpha")
 
 
-def to_device(s, device="cuda") -> dict:
-    """scenegen.Surfels (numpy fp32) -> dict of contiguous CUDA tensors."""
+def to_device(s, device="cuda", bounds: bool = True) -> dict:
+    """scenegen.Surfels (numpy fp32) -> dict of contiguous CUDA tensors
+    (+ the block bounds of the hierarchical cull, gs_cull_bounds, unless
+    bounds=False)."""
     f = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
-    return dict(means=f(s.means), quats=f(s.quats), scales=f(s.scales), opacities=f(s.opacities),
-                sh=f(s.sh), sh_degree=int(s.sh_degree), intensity=f(s.intensity),
-                raydrop_logit=f(s.raydrop_logit))
+    d = dict(means=f(s.means), quats=f(s.quats), scales=f(s.scales), opacities=f(s.opacities),
+             sh=f(s.sh), sh_degree=int(s.sh_degree), intensity=f(s.intensity),
+             raydrop_logit=f(s.raydrop_logit))
+    if bounds:
+        cull_bounds(d)
+    return d
+
+
+def cull_bounds(surfels: dict, stream=None, n: int | None = None) -> torch.Tensor:
+    """Compute (gs_cull_bounds, on `stream`: a raw CUDA stream handle, default
+    the current stream) the block bounds of the first n surfels (default all)
+    of a to_device dict into surfels["cull_bounds"] (allocated on first use,
+    sized for the whole buffers).  Call again whenever means or scales change."""
+    means = surfels["means"]
+    b = surfels.get("cull_bounds")
+    if b is None:
+        b = torch.empty((max(gsr.gs_cull_blocks(means.shape[0]), 1), 8), dtype=torch.float32, device=means.device)
+        surfels["cull_bounds"] = b
+    st = stream if stream is not None else torch.cuda.current_stream(means.device).cuda_stream
+    view = {k: (v[: n] if (n is not None and isinstance(v, torch.Tensor) and k != "cull_bounds") else v)
+            for k, v in surfels.items() if k != "cull_bounds"}
+    gsr.gs_cull_bounds(gsr.surfels_struct(view), b, st)
+    return b
 
 
 def n_channels(kind):

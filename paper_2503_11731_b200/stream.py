@@ -29,6 +29,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import gsr, render
+
 FIELDS = ("means", "quats", "scales", "opacities", "sh", "intensity", "raydrop_logit")
 
 
@@ -91,14 +93,17 @@ class ChunkStreamer:
 
     def _alloc(self, n):
         h = self.host[0]
-        return {f: (None if h[f] is None else torch.empty((n,) + tuple(h[f].shape[1:]), dtype=torch.float32,
-                                                          device=self.device)) for f in FIELDS}
+        b = {f: (None if h[f] is None else torch.empty((n,) + tuple(h[f].shape[1:]), dtype=torch.float32,
+                                                       device=self.device)) for f in FIELDS}
+        b["cull_bounds"] = torch.empty((max(gsr.gs_cull_blocks(n), 1), 8), dtype=torch.float32, device=self.device)
+        return b
 
     def _view(self, i):
         ids = self.sets[i]
         n = sum(self.counts[c] for c in ids) if ids is not None else 0
-        d = {f: (None if t is None else t[:n]) for f, t in self.buf[i].items()}
+        d = {f: (None if t is None else t[:n]) for f, t in self.buf[i].items() if f != "cull_bounds"}
         d["sh_degree"] = self.sh_degree
+        d["cull_bounds"] = self.buf[i]["cull_bounds"]   # of the first n surfels (computed by _upload)
         return d
 
     def front(self) -> dict:
@@ -136,7 +141,15 @@ class ChunkStreamer:
         ev = self._upload(self.front_i, ids)
         ev.synchronize()
         self.sets[self.front_i] = ids
+        self._bounds(self.front_i)
         return ids
+
+    def _bounds(self, i):
+        """Block bounds of buffer i's set (hierarchical cull, gs_cull_bounds), on the
+        current stream once the upload is complete: a kernel queued behind the copy
+        stream's transfers would hold up other streams sharing its hardware queue."""
+        n = sum(self.counts[c] for c in self.sets[i])
+        render.cull_bounds(dict(self.buf[i], sh_degree=self.sh_degree), n=n)
 
     def update(self, position) -> bool:
         """Start uploading the pose's active set into the back buffer if it
@@ -164,6 +177,7 @@ class ChunkStreamer:
             return False
         torch.cuda.current_stream(self.device).wait_event(ev)
         self.sets[back] = ids
+        self._bounds(back)
         self.front_i = back
         self.pending = None
         self.swaps += 1

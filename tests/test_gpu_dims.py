@@ -212,6 +212,62 @@ def test_binning_bit_exact_full_chunked_forward_frame(gsr_mod):
     assert not np.any(cul[vis])
 
 
+# ---------------------------------------------------------------- hierarchical cull (gs_cull_bounds)
+def _project_state(r, se):
+    """Candidate list and per-surfel outputs of gs_project, as numpy."""
+    proj, d_np = r.project(se)
+    torch.cuda.synchronize()
+    hdr = proj[:16].view(torch.int32).cpu().tolist()
+    n_vis, n_cand = hdr[0], hdr[1]
+    from paper_2503_11731_b200 import gsr
+    import ctypes as C
+    offs = (C.c_size_t * 5)()
+    gsr.load().gs_projected_offsets(r.n, int(se.kind), offs)
+    cnt = proj[offs[3]: offs[3] + 4 * r.n].view(torch.int32).cpu().numpy()
+    key = proj[offs[2]: offs[2] + 4 * r.n].view(torch.int32).cpu().numpy()
+    return n_vis, n_cand, int(d_np.item()), cnt, key
+
+
+@pytest.mark.parametrize("case", ["street", "invalid"])
+def test_block_bounds_cull_is_bitwise_the_per_surfel_cull(gsr_mod, case):
+    """gs_project with gs_cull_bounds' block bounds (zone-wise
+    resident sets) gives exactly the candidates, counts, keys, pair total and
+    image of gs_project without them: six surround pinholes over a street of
+    four 50 m zones stored zone by zone (whole blocks fall outside each
+    frustum), with NaN / Inf centres and invalid scales mixed in."""
+    from paper_2503_11731_b200 import gsr
+    from paper_2503_11731_b200.render import Renderer, to_device
+    parts = [sg.street(np.random.default_rng(40 + c), 30_000, 50.0 * c, 50.0 * c + 50.0, 1) for c in range(4)]
+    s = sg.Surfels.concat(parts)
+    if case == "invalid":
+        rng = np.random.default_rng(9)
+        idx = rng.choice(s.n, 600, replace=False)
+        s.means[idx[:100], 0] = np.nan
+        s.means[idx[100:200], 2] = np.inf
+        s.means[idx[200:300], 1] = -np.inf
+        s.scales[idx[300:400], 0] = np.inf
+        s.scales[idx[400:500], 1] = np.nan
+        s.scales[idx[500:600]] = 0.0
+    with_b, without = to_device(s), to_device(s, bounds=False)
+    assert with_b["cull_bounds"].shape == (gsr.gs_cull_blocks(s.n), 8) and "cull_bounds" not in without
+    ra, rb = Renderer(with_b), Renderer(without)
+    skipped = 0
+    for z in (20.0, 75.0, 130.0, 199.0):
+        for yaw in sg.CHUNKED_CAM_YAWS:
+            se = gsr.Sensor(sg.pinhole(320, 180, 200.0, 160.0, 90.0, sg.camera_pose([0.0, 1.5, z], math.radians(yaw))))
+            a, b = _project_state(ra, se), _project_state(rb, se)
+            assert a[:3] == b[:3], (z, yaw, a[:3], b[:3])
+            np.testing.assert_array_equal(a[3], b[3])
+            vis = b[3] > 0
+            np.testing.assert_array_equal(a[4][vis], b[4][vis])
+            skipped += int(b[1] < s.n // 2)
+    assert skipped > 0
+    se = sg.pinhole(320, 180, 200.0, 160.0, 90.0, sg.camera_pose([0.0, 1.5, 75.0], math.radians(60.0)))
+    ia, ib = ra.render(se), rb.render(se)
+    torch.cuda.synchronize()
+    assert torch.equal(ia, ib)
+
+
 # ---------------------------------------------------------------- cylindrical fisheye (Eq. 4, NEXT-4)
 @pytest.mark.parametrize("hfov,yaw", [(300.0, 0.0), (200.0, 70.0), (90.0, -30.0)])
 def test_cylindrical_fisheye_full_frame(gsr_mod, hfov, yaw):
