@@ -367,6 +367,30 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
 }
 
 // ------------------------------------------------------------------ cull
+// Per-sensor constants of cull_one (the same fp32 expressions it used to
+// evaluate per surfel -- IEEE divisions and square roots -- computed once per
+// thread: k_cull<pinhole> 3080 -> 1650 SASS instructions per 8-surfel thread).
+struct CullConst {
+    float kR;                       // 1.001 sqrt(support 1.0001 + 1e-4)
+    float xl, xr, yl, yr;           // frustum side slopes with the pixel margin (pinhole)
+    float nxl, nxr, nyl, nyr;       // sqrt(1 + slope^2)
+};
+template <int KIND>
+__device__ __forceinline__ CullConst make_cull_const(const DevSensor &se, const DevOpts &op) {
+    CullConst c;
+    c.kR = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f);
+    c.xl = c.xr = c.yl = c.yr = c.nxl = c.nxr = c.nyl = c.nyr = 0.f;
+    if (KIND == GS_PINHOLE) {
+        // margin: the low-pass disc radius sqrt(rcut) sigma (the same cut as k_project) + 1 px
+        const float m = 1.f + sqrtf(op.support * 1.0001f + 1e-4f) * sqrtf(op.sigma2);
+        c.xl = (-m - se.cx) / se.fx; c.xr = ((float)se.width + m - se.cx) / se.fx;
+        c.yl = (-m - se.cy) / se.fy; c.yr = ((float)se.height + m - se.cy) / se.fy;
+        c.nxl = sqrtf(1.f + c.xl * c.xl); c.nxr = sqrtf(1.f + c.xr * c.xr);
+        c.nyl = sqrtf(1.f + c.yl * c.yl); c.nyr = sqrtf(1.f + c.yr * c.yr);
+    }
+    return c;
+}
+
 // Conservative cull ahead of the fp64 projection: a surfel is dropped when
 // its centre fails the depth-key test (exact, the same pinned key as
 // k_project) or when the sphere of radius 3.001 max(s_u, s_v) around its
@@ -379,9 +403,17 @@ __device__ void angular_box_cap(const double m[3], double beta, AngBox &ab) {
 // surfel provably meets no sample ray, so this only skips work -- k_project
 // takes every decision for the surfels that pass.  Passing surfels are compacted in index order
 // (decoupled look-back); the others get the culled outputs here.
+// sqrt.approx (2 ulp) for the cull's conservative bounds: every use below is
+// compared with margins of 1e-4 (1 + r) m or 1 % -- far above 2 ulp.
+__device__ __forceinline__ float sqrt_apx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 template <int KIND>
-__device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op, int64_t i,
-                                         uint32_t &keybits, const float *sb) {
+__device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &se, const DevOpts &op,
+                                         const CullConst &cc, int64_t i, uint32_t &keybits, const float *sb) {
     const float mx = __ldg(s.means + 3 * i), my = __ldg(s.means + 3 * i + 1), mz = __ldg(s.means + 3 * i + 2);
     const float X = fmaf(se.R[0], mx, fmaf(se.R[1], my, fmaf(se.R[2], mz, se.t[0])));
     const float Y = fmaf(se.R[3], mx, fmaf(se.R[4], my, fmaf(se.R[5], mz, se.t[1])));
@@ -390,29 +422,24 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
     // fp64 key, reading R9) to the candidates; the margin covers the fp32 rounding here
     const float mag = fabsf(mx) + fabsf(my) + fabsf(mz) + fabsf(se.t[0]) + fabsf(se.t[1]) + fabsf(se.t[2]);
     const float nearm = op.near_plane - fmaf(1e-5f, mag, 1e-6f);
-    const float keyf = KIND == GS_PINHOLE ? Z : sqrtf(fmaf(X, X, fmaf(Y, Y, Z * Z)));
+    const float keyf = KIND == GS_PINHOLE ? Z : sqrt_apx(fmaf(X, X, fmaf(Y, Y, Z * Z)));
     keybits = __float_as_uint(keyf);
     const float o = __ldg(s.opac + i);
     const float2 sc = __ldg(reinterpret_cast<const float2 *>(s.scales) + i);
     if (!(keyf >= nearm) || !(o > 0.f) || !(sc.x > 0.f) || !(sc.y > 0.f) || !isfinite(sc.x) ||
         !isfinite(sc.y))
         return false;
-    const float R = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f) * fmaxf(sc.x, sc.y) +
-                    1e-3f * (1.f + fabsf(X) + fabsf(Y) + fabsf(Z));
+    const float R = cc.kR * fmaxf(sc.x, sc.y) + 1e-3f * (1.f + fabsf(X) + fabsf(Y) + fabsf(Z));
     if (!isfinite(X + Y + Z + R)) return true;   // let k_project decide
     if (KIND == GS_PINHOLE) {
-        // margin: the low-pass disc radius sqrt(rcut) sigma (the same cut as k_project) + 1 px
-        const float m = 1.f + sqrtf(op.support * 1.0001f + 1e-4f) * sqrtf(op.sigma2);
-        const float xl = (-m - se.cx) / se.fx, xr = ((float)se.width + m - se.cx) / se.fx;
-        const float yl = (-m - se.cy) / se.fy, yr = ((float)se.height + m - se.cy) / se.fy;
-        if ((X - xl * Z) < -R * sqrtf(1.f + xl * xl)) return false;
-        if ((xr * Z - X) < -R * sqrtf(1.f + xr * xr)) return false;
-        if ((Y - yl * Z) < -R * sqrtf(1.f + yl * yl)) return false;
-        if ((yr * Z - Y) < -R * sqrtf(1.f + yr * yr)) return false;
+        if ((X - cc.xl * Z) < -R * cc.nxl) return false;
+        if ((cc.xr * Z - X) < -R * cc.nxr) return false;
+        if ((Y - cc.yl * Z) < -R * cc.nyl) return false;
+        if ((cc.yr * Z - Y) < -R * cc.nyr) return false;
         return true;
     }
     if (KIND == GS_FISHEYE_CYLINDRICAL) return true;   // no field-of-view pre-cull: k_project's box decides
-    const float r = sqrtf(X * X + Y * Y + Z * Z);
+    const float r = sqrt_apx(X * X + Y * Y + Z * Z);
     if (!(r > R * 1.01f)) return true;
     if (KIND == GS_FISHEYE_EQUIDISTANT) {
         const float beta = asinf(R / r);
@@ -433,10 +460,10 @@ __device__ __forceinline__ bool cull_one(const DevSurfels &s, const DevSensor &s
     const float tv0 = 2.f * (qx * qy - qw * qz), tv1 = 1.f - 2.f * (qx * qx + qz * qz), tv2 = 2.f * (qy * qz + qw * qx);
     const float az = se.R[6] * tu0 + se.R[7] * tu1 + se.R[8] * tu2;
     const float bz = se.R[6] * tv0 + se.R[7] * tv1 + se.R[8] * tv2;
-    const float Rr = R / fmaxf(sc.x, sc.y);   // 1.001 sqrt(rcut) (+ the absolute margin, scaled)
+    const float Rr = __fdividef(R, fmaxf(sc.x, sc.y));   // 1.001 sqrt(rcut) (+ the absolute margin, scaled)
     const float mg = 1e-4f * (1.f + r);
-    const float hz = Rr * sqrtf((sc.x * az) * (sc.x * az) + (sc.y * bz) * (sc.y * bz)) + mg;
-    const float rxy = sqrtf(X * X + Y * Y);
+    const float hz = Rr * sqrt_apx((sc.x * az) * (sc.x * az) + (sc.y * bz) * (sc.y * bz)) + mg;
+    const float rxy = sqrt_apx(X * X + Y * Y);
     const float rlo = rxy - R - mg, rhi = rxy + R + mg;
     if (!(rlo > 1e-3f * r)) return true;   // near the vertical axis: keep
     const float zlo = Z - hz, zhi = Z + hz;
@@ -510,7 +537,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_bounds(const float *__restrict
 // with twice cull_one's own fp32 margin to spare; every comparison is false
 // on a NaN, so a block with non-finite bounds is never rejected.
 __device__ __forceinline__ bool block_outside(const float *__restrict__ bnd, const DevSensor &se,
-                                              const DevOpts &op) {
+                                              const DevOpts &op, const CullConst &cc) {
     const float4 b0 = __ldg(reinterpret_cast<const float4 *>(bnd)), b1 = __ldg(reinterpret_cast<const float4 *>(bnd) + 1);
     const float c[3] = {0.5f * (b0.x + b0.w), 0.5f * (b0.y + b1.x), 0.5f * (b0.z + b1.y)};
     // half extents, rounded up (the centre above is rounded too)
@@ -529,15 +556,12 @@ __device__ __forceinline__ bool block_outside(const float *__restrict__ bnd, con
     const float slack = 3e-3f * (1.f + mags) + 3e-5f * magw;   // > 2x cull_one's margins + this function's rounding
     // near plane: cull_one drops Z < near - (1e-5 mag + 1e-6)
     if (Xc[2] + Xe[2] < op.near_plane - slack) return true;
-    const float R = 1.001f * sqrtf(op.support * 1.0001f + 1e-4f) * b1.z + slack;   // >= every surfel's R
-    const float m = 1.f + sqrtf(op.support * 1.0001f + 1e-4f) * sqrtf(op.sigma2);
-    const float xl = (-m - se.cx) / se.fx, xr = ((float)se.width + m - se.cx) / se.fx;
-    const float yl = (-m - se.cy) / se.fy, yr = ((float)se.height + m - se.cy) / se.fy;
+    const float R = cc.kR * b1.z + slack;   // >= every surfel's R
     // f(X) = a X + b Y + g Z over the block: f(Xc) + |a| Xe_x + |b| Xe_y + |g| Xe_z
-    if ((Xc[0] - xl * Xc[2]) + Xe[0] + fabsf(xl) * Xe[2] < -R * sqrtf(1.f + xl * xl) - slack) return true;
-    if ((xr * Xc[2] - Xc[0]) + Xe[0] + fabsf(xr) * Xe[2] < -R * sqrtf(1.f + xr * xr) - slack) return true;
-    if ((Xc[1] - yl * Xc[2]) + Xe[1] + fabsf(yl) * Xe[2] < -R * sqrtf(1.f + yl * yl) - slack) return true;
-    if ((yr * Xc[2] - Xc[1]) + Xe[1] + fabsf(yr) * Xe[2] < -R * sqrtf(1.f + yr * yr) - slack) return true;
+    if ((Xc[0] - cc.xl * Xc[2]) + Xe[0] + fabsf(cc.xl) * Xe[2] < -R * cc.nxl - slack) return true;
+    if ((cc.xr * Xc[2] - Xc[0]) + Xe[0] + fabsf(cc.xr) * Xe[2] < -R * cc.nxr - slack) return true;
+    if ((Xc[1] - cc.yl * Xc[2]) + Xe[1] + fabsf(cc.yl) * Xe[2] < -R * cc.nyl - slack) return true;
+    if ((cc.yr * Xc[2] - Xc[1]) + Xe[1] + fabsf(cc.yr) * Xe[2] < -R * cc.nyr - slack) return true;
     return false;
 }
 
@@ -561,13 +585,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cull(DevSurfels s, const __gri
     uint32_t flags = 0, cnt = 0;
     // hierarchical cull: a block wholly outside the frustum skips the per-surfel pass
     // (its surfels still get their zero counts and the tile its place in the look-back)
-    const bool skip = KIND == GS_PINHOLE && s.bounds && block_outside(s.bounds + (size_t)tile * 8, se, op);
+    const CullConst cc = make_cull_const<KIND>(se, op);
+    const bool skip = KIND == GS_PINHOLE && s.bounds && block_outside(s.bounds + (size_t)tile * 8, se, op, cc);
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         const int64_t i = base + j * SCAN_THREADS + threadIdx.x;
         if (i < s.n) {
             uint32_t kb;
-            const bool c = !skip && cull_one<KIND>(s, se, op, i, kb, sb);
+            const bool c = !skip && cull_one<KIND>(s, se, op, cc, i, kb, sb);
             if (c) { flags |= 1u << j; ++cnt; }
             // every surfel gets a zero pair count here (coalesced); k_project writes
             // count, key and rect of every candidate.  Nothing reads the key or rect
