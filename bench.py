@@ -604,7 +604,7 @@ def main():
     ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
     ap.add_argument("--workload", default="chunked", choices=["chunked", "mid", "fisheye", "lidar", "tiny"])
     ap.add_argument("--timesteps", type=int, default=64)
-    ap.add_argument("--streams", type=int, default=10)
+    ap.add_argument("--streams", type=int, default=14)
     ap.add_argument("--grid-share", type=float, default=None,
                     help="gs_opts.grid_share of every frame (default: BatchRenderer's 2/streams)")
     ap.add_argument("--priority", choices=["none", "pre", "comp"], default="comp",

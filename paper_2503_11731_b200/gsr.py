@@ -205,7 +205,15 @@ def surfels_struct(t: dict) -> gs_surfels:
     s.sh_degree = int(t.get("sh_degree", 0))
     s.intensity = t["intensity"].data_ptr() if t.get("intensity") is not None else None
     s.raydrop_logit = t["raydrop_logit"].data_ptr() if t.get("raydrop_logit") is not None else None
-    s.cull_bounds = t["cull_bounds"].data_ptr() if t.get("cull_bounds") is not None else None
+    b = t.get("cull_bounds")
+    if b is not None:
+        # the bounds describe exactly these arrays (gsr.h): a sliced or regrouped dict must drop or recompute them
+        if b.dim() != 2 or b.shape[1] != 8 or b.shape[0] < gs_cull_blocks(s.n) or not b.is_contiguous():
+            raise ValueError(f"cull_bounds of shape {tuple(b.shape)} cannot describe {s.n} surfels "
+                             "(recompute with render.cull_bounds or drop the key)")
+        s.cull_bounds = b.data_ptr()
+    else:
+        s.cull_bounds = None
     return s
 
 

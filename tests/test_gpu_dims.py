@@ -266,6 +266,14 @@ def test_block_bounds_cull_is_bitwise_the_per_surfel_cull(gsr_mod, case):
     ia, ib = ra.render(se), rb.render(se)
     torch.cuda.synchronize()
     assert torch.equal(ia, ib)
+    if case == "invalid":   # blocks holding an infinite centre have infinite bounds and are never skipped
+        return
+    # the block path is live: bounds that put every block far behind a forward camera cull everything
+    fwd = gsr.Sensor(sg.pinhole(320, 180, 200.0, 160.0, 90.0, sg.camera_pose([0.0, 1.5, 75.0], 0.0)))
+    assert _project_state(ra, fwd)[1] > 0
+    with_b["cull_bounds"][:, 2] = -1000.0
+    with_b["cull_bounds"][:, 5] = -900.0
+    assert _project_state(ra, fwd)[1] == 0
 
 
 # ---------------------------------------------------------------- cylindrical fisheye (Eq. 4, NEXT-4)
