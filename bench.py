@@ -296,7 +296,7 @@ def run_gsr(args):
 
     surf = to_device(surfels_np, device)
     br = BatchRenderer(surf, device=device, n_streams=args.streams, grid_share=args.grid_share,
-                       priority=None if args.priority == "none" else args.priority)
+                       priority=None if args.priority == "none" else args.priority, deal=args.deal)
     caps, contrib, evals = br.plan(my_sensors, stats=True)
     sensors = br.wrap(my_sensors)
 
@@ -574,7 +574,7 @@ def run_gsr(args):
 
     if rank == 0:
         desc.update(parallelism=f"frame-shard{world} (timestep blocks, surfels replicated, NCCL p2p gather to rank 0)"
-                    if world > 1 else "1 GPU", streams=args.streams, priority=args.priority, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
+                    if world > 1 else "1 GPU", streams=args.streams, deal=args.deal, priority=args.priority, grid_share=round(br.lanes[0].cam_opts.grid_share, 4),
                     cuda_graph=graph_note,
                     l2="no flush: resident surfels (%.2f GB) and outputs (%.1f GB) exceed the 126 MB L2" % (
                         sum(v.numel() * 4 for v in surf.values() if isinstance(v, torch.Tensor)) / 1e9,
@@ -610,6 +610,9 @@ def main():
     ap.add_argument("--priority", choices=["none", "pre", "comp"], default="comp",
                     help="per-lane stream priorities: projection + binning (pre) or compositing (comp) "
                          "on a higher-priority stream; none: one stream per lane")
+    ap.add_argument("--deal", choices=["round_robin", "balanced"], default="round_robin",
+                    help="how frames are dealt to lanes: frame i on lane i %% lanes, or each frame to the lane "
+                         "with the least planned work (pairs) so far")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-frame rates")

@@ -43,7 +43,7 @@ class FrameTimes:
 class BatchRenderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
                  lidar_tile=(32, 1), grid_share: float | None = None, big_tile=(16, 16),
-                 big_tile_ratio: float = 16.0, priority: str | None = "comp"):
+                 big_tile_ratio: float = 16.0, priority: str | None = "comp", deal: str = "round_robin"):
         """grid_share: fraction of the GPU's resident compositor CTA slots each
         frame's persistent grid takes (gs_opts.grid_share); default 2/n_streams
         (capped at 1), so about two frames composite at once and the other
@@ -60,6 +60,9 @@ class BatchRenderer:
         stream priority (Chunked batch, 10 lanes: none 992, pre 1003, comp
         1010 Msamples/s)."""
         self.device = torch.device(device)
+        assert deal in ("round_robin", "balanced"), deal
+        self.deal = deal        # how render() deals frames to lanes (see plan())
+        self.lane_of = None
         n_streams = max(1, n_streams)
         o = gsr.gs_opts.from_buffer_copy(opts) if opts is not None else gsr.default_opts()
         o.grid_share = float(grid_share) if grid_share is not None else min(1.0, 2.0 / n_streams)
@@ -114,6 +117,21 @@ class BatchRenderer:
             fopts.append(o)
         self.caps = caps
         self.frame_opts = fopts
+        # deal frames to lanes: round robin (frame i on lane i % lanes), or balanced -- in
+        # frame order, each frame to the lane with the least planned work so far (a frame's
+        # work ~ 4.3 M pair-equivalents of fixed cost + its pairs: Chunked forward / side /
+        # LiDAR frames take 4.0 / 1.4 / 2.4 ms for 27.2 / 6.6 / 11.3 M pairs), so lanes do
+        # not specialise on one frame type when the lane count is a multiple of the
+        # per-timestep frame count
+        if self.deal == "balanced":
+            load = [0.0] * len(self.lanes)
+            self.lane_of = []
+            for P in caps:
+                k = min(range(len(load)), key=lambda j: (load[j], j))
+                load[k] += 4.3e6 + P
+                self.lane_of.append(k)
+        else:
+            self.lane_of = [i % len(self.lanes) for i in range(len(caps))]
         self.ovf = torch.zeros(len(sensors), dtype=torch.int32, device=self.device)
         if stats:
             for s, cap, o in zip(sensors, caps, fopts):
@@ -126,7 +144,7 @@ class BatchRenderer:
         return (caps, contrib, evals) if stats else caps
 
     def render(self, sensors, outs, times: FrameTimes | None = None, on_frame=None, event_log: list | None = None):
-        """Render frame i into outs[i] on lane i % n_streams.  times: if given,
+        """Render frame i into outs[i] on lane lane_of[i] (plan()).  times: if given,
         per-frame event durations are appended after the batch completes
         (this synchronises).  event_log: if given, each frame's 4 CUDA events
         (before gs_project, gs_bin_sort, the render call, after it) are
@@ -143,7 +161,7 @@ class BatchRenderer:
                 st.wait_stream(cur)
         evs = []
         for i, s in enumerate(sensors):
-            k = i % len(self.lanes)
+            k = self.lane_of[i]
             want = times is not None or event_log is not None
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if want else None
             rs = self.rstreams[k]

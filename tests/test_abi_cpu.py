@@ -173,3 +173,35 @@ def test_decode_kernel_uses_tcgen05():
     dec = [f for f in funcs if f.startswith("_ZN3gsr3dec8k_decode")]
     assert len(dec) == 2   # camera and LiDAR instantiations
     assert all("UTCHMMA" in f and "LDTM" in f for f in dec)
+
+
+def test_cull_bounds_validation():
+    """gs_cull_bounds / gs_cull_blocks (hierarchical cull): argument
+    checks run before any launch, and the binding refuses block bounds that
+    cannot describe the surfel arrays they travel with."""
+    import torch
+    from paper_2503_11731_b200 import gsr
+    lib = gsr.load()
+    assert gsr.gs_cull_blocks(0) == 0 and gsr.gs_cull_blocks(1) == 1
+    assert gsr.gs_cull_blocks(2048) == 1 and gsr.gs_cull_blocks(2049) == 2
+    sf = gsr.gs_surfels()
+    assert lib.gs_cull_bounds(None, None, None) == gsr.GS_ERR_CONFIG
+    sf.n = -1
+    assert lib.gs_cull_bounds(C.byref(sf), None, None) == gsr.GS_ERR_RANGE
+    sf.n = 0
+    assert lib.gs_cull_bounds(C.byref(sf), None, None) == gsr.GS_OK     # nothing to do
+    sf.n = 10
+    assert lib.gs_cull_bounds(C.byref(sf), None, None) == gsr.GS_ERR_CONFIG
+    sf.means, sf.scales = 16, 20                                          # scales misaligned
+    assert lib.gs_cull_bounds(C.byref(sf), C.c_void_p(32), None) == gsr.GS_ERR_CONFIG
+    sf.scales = 24
+    assert lib.gs_cull_bounds(C.byref(sf), C.c_void_p(40), None) == gsr.GS_ERR_CONFIG   # bounds misaligned
+    t = dict(means=torch.zeros(5000, 3), quats=torch.zeros(5000, 4), scales=torch.zeros(5000, 2),
+             opacities=torch.zeros(5000), cull_bounds=torch.zeros(3, 8))
+    assert gsr.surfels_struct(t).cull_bounds is not None
+    for bad in (torch.zeros(2, 8), torch.zeros(3, 7), torch.zeros(24)):
+        t["cull_bounds"] = bad
+        with pytest.raises(ValueError):
+            gsr.surfels_struct(t)
+    del t["cull_bounds"]
+    assert gsr.surfels_struct(t).cull_bounds is None
