@@ -296,7 +296,8 @@ def run_gsr(args):
 
     surf = to_device(surfels_np, device)
     br = BatchRenderer(surf, device=device, n_streams=args.streams, grid_share=args.grid_share,
-                       priority=None if args.priority == "none" else args.priority, deal=args.deal)
+                       priority=None if args.priority == "none" else args.priority, deal=args.deal,
+                       heavy_share=args.heavy_share)
     caps, contrib, evals = br.plan(my_sensors, stats=True)
     sensors = br.wrap(my_sensors)
 
@@ -613,6 +614,8 @@ def main():
     ap.add_argument("--deal", choices=["round_robin", "balanced"], default="round_robin",
                     help="how frames are dealt to lanes: frame i on lane i %% lanes, or each frame to the lane "
                          "with the least planned work (pairs) so far")
+    ap.add_argument("--heavy-share", type=float, default=None,
+                    help="grid_share of frames with more than 1.5x the batch's mean pair count (default: as the others)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-frame rates")

@@ -43,7 +43,8 @@ class FrameTimes:
 class BatchRenderer:
     def __init__(self, surfels: dict, opts: gsr.gs_opts | None = None, device="cuda", n_streams: int = 2,
                  lidar_tile=(32, 1), grid_share: float | None = None, big_tile=(16, 16),
-                 big_tile_ratio: float = 16.0, priority: str | None = "comp", deal: str = "round_robin"):
+                 big_tile_ratio: float = 16.0, priority: str | None = "comp", deal: str = "round_robin",
+                 heavy_share: float | None = None):
         """grid_share: fraction of the GPU's resident compositor CTA slots each
         frame's persistent grid takes (gs_opts.grid_share); default 2/n_streams
         (capped at 1), so about two frames composite at once and the other
@@ -60,6 +61,7 @@ class BatchRenderer:
         stream priority (Chunked batch, 10 lanes: none 992, pre 1003, comp
         1010 Msamples/s)."""
         self.device = torch.device(device)
+        self.heavy_share = heavy_share   # grid_share of frames with > 1.5x the batch's mean pairs (None: as the others)
         assert deal in ("round_robin", "balanced"), deal
         self.deal = deal        # how render() deals frames to lanes (see plan())
         self.lane_of = None
@@ -115,6 +117,13 @@ class BatchRenderer:
                     P = int(d_np.item())
             caps.append(P)
             fopts.append(o)
+        if self.heavy_share is not None and caps:
+            mean = sum(caps) / len(caps)
+            for i, P in enumerate(caps):
+                if P > 1.5 * mean:
+                    o = gsr.gs_opts.from_buffer_copy(fopts[i] if fopts[i] is not None else self.lanes[0].opts_for(sensors[i]))
+                    o.grid_share = float(self.heavy_share)
+                    fopts[i] = o
         self.caps = caps
         self.frame_opts = fopts
         # deal frames to lanes: round robin (frame i on lane i % lanes), or balanced -- in
