@@ -611,7 +611,7 @@ def main():
     ap.add_argument("--priority", choices=["none", "pre", "comp"], default="comp",
                     help="per-lane stream priorities: projection + binning (pre) or compositing (comp) "
                          "on a higher-priority stream; none: one stream per lane")
-    ap.add_argument("--deal", choices=["round_robin", "balanced"], default="round_robin",
+    ap.add_argument("--deal", choices=["round_robin", "balanced", "typed"], default="round_robin",
                     help="how frames are dealt to lanes: frame i on lane i %% lanes, or each frame to the lane "
                          "with the least planned work (pairs) so far")
     ap.add_argument("--heavy-share", type=float, default=None,

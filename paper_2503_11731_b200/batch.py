@@ -62,7 +62,7 @@ class BatchRenderer:
         1010 Msamples/s)."""
         self.device = torch.device(device)
         self.heavy_share = heavy_share   # grid_share of frames with > 1.5x the batch's mean pairs (None: as the others)
-        assert deal in ("round_robin", "balanced"), deal
+        assert deal in ("round_robin", "balanced", "typed"), deal
         self.deal = deal        # how render() deals frames to lanes (see plan())
         self.lane_of = None
         n_streams = max(1, n_streams)
@@ -139,6 +139,38 @@ class BatchRenderer:
                 k = min(range(len(load)), key=lambda j: (load[j], j))
                 load[k] += 4.3e6 + P
                 self.lane_of.append(k)
+        elif self.deal == "typed":
+            # lanes specialise on a frame class (sensor kind, tile shape, pair count to a
+            # power of two) and every class gets lanes in proportion to its planned work;
+            # inside a class frames go round robin over the class's lanes
+            import math
+            cls = [(int(s.kind), fopts[i] is not None, int(round(math.log2(max(P, 1)))))
+                   for i, (s, P) in enumerate(zip(sensors, caps))]
+            work = {}
+            for c, P in zip(cls, caps):
+                work[c] = work.get(c, 0.0) + 4.3e6 + P
+            L = len(self.lanes)
+            keys = sorted(work, key=lambda c: -work[c])[:L]        # more classes than lanes: the lightest share
+            tot = sum(work[c] for c in keys)
+            share = {c: max(1, int(work[c] / tot * L)) for c in keys}
+            while sum(share.values()) > L:
+                c = max(share, key=lambda c: (share[c] > 1, share[c] - work[c] / tot * L))
+                share[c] -= 1
+            while sum(share.values()) < L:
+                c = max(share, key=lambda c: work[c] / share[c])
+                share[c] += 1
+            first, nxt = {}, 0
+            for c in keys:
+                first[c] = nxt
+                nxt += share[c]
+            seen = {}
+            self.lane_of = []
+            for c in cls:
+                if c not in first:
+                    c = keys[-1]
+                j = seen.get(c, 0)
+                seen[c] = j + 1
+                self.lane_of.append(first[c] + j % share[c])
         else:
             self.lane_of = [i % len(self.lanes) for i in range(len(caps))]
         self.ovf = torch.zeros(len(sensors), dtype=torch.int32, device=self.device)
